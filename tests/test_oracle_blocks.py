@@ -1,0 +1,215 @@
+"""Pins of oracle/blocks.py (the block method's intermediate objects).
+
+Hand-derived examples (worked in the comments, SPEC.md-style), the block method's
+correctness theorem (sum of per-task counts = T from the node iterator and brute
+force), and structural invariants.
+"""
+import itertools
+from math import comb
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import oracle.blocks as ob
+
+
+# ---- S1 canonicalise ---------------------------------------------------------------
+def test_canonical_vs_set():
+    n, s, d = gen.messy(gen.rmat(8, 8, 3), seed=2)
+    E = ob.canonical_edges(n, s, d)
+    ref = sorted({(min(int(a), int(b)), max(int(a), int(b))) for a, b in zip(s, d) if a != b})
+    assert [tuple(map(int, e)) for e in E] == ref
+
+
+# ---- S2 degree order (SPEC.md degree_relabel examples) ------------------------------
+def test_rank_star_hub_last():
+    n, s, d = gen.star(5)
+    E = ob.canonical_edges(n, s, d)
+    r = ob.degree_rank(n, ob.degrees(n, E))
+    assert r[0] == n - 1
+
+
+def test_rank_ring_identity():
+    n, s, d = gen.cycle(7)
+    E = ob.canonical_edges(n, s, d)
+    assert (ob.degree_rank(n, ob.degrees(n, E)) == np.arange(7)).all()
+
+
+def test_rank_p4_ties_by_id():
+    # P4 degrees [1,2,2,1] -> order 0,3,1,2 -> rank = [0,2,3,1]
+    n, s, d = gen.path(4)
+    E = ob.canonical_edges(n, s, d)
+    assert list(ob.degree_rank(n, ob.degrees(n, E))) == [0, 2, 3, 1]
+
+
+# ---- S3 orient -------------------------------------------------------------------
+def test_dag_half_edges_low_to_high():
+    g = gen.rmat(9, 16, 1)
+    E = ob.canonical_edges(*g)
+    rank = ob.degree_rank(g[0], ob.degrees(g[0], E))
+    D = ob.dag(E, rank)
+    assert D.shape == E.shape
+    assert (D[:, 0] < D[:, 1]).all()
+    assert len({tuple(x) for x in D}) == len(D)
+
+
+# ---- S4 cuts: hand examples ----------------------------------------------------------
+def _plan_objs(g, p, rule=0):
+    n = g[0]
+    E = ob.canonical_edges(*g)
+    rank = ob.degree_rank(n, ob.degrees(n, E))
+    D = ob.dag(E, rank)
+    return n, D, ob.cuts(n, D, p, rule)
+
+
+def test_cuts_p4_hand():
+    # P4: DAG (rank space) (0,2),(1,3),(2,3); d+=[1,1,1,0], d-=[0,0,1,2]
+    # rule 0 weights [1,1,2,0], P=[0,1,2,4,4]: p=2 -> [0,2,4]; p=3 -> [0,2,3,4]
+    # rule 1 weights [1,1,1,0], P=[0,1,2,3,3]: p=2 -> 2P>=3 -> c=2
+    g = gen.path(4)
+    assert list(_plan_objs(g, 2, 0)[2]) == [0, 2, 4]
+    assert list(_plan_objs(g, 3, 0)[2]) == [0, 2, 3, 4]
+    assert list(_plan_objs(g, 2, 1)[2]) == [0, 2, 4]
+
+
+def test_cuts_p1_and_clamp():
+    g = gen.rmat(7, 8, 1)
+    assert list(_plan_objs(g, 1)[2]) == [0, g[0]]
+    n, D, c = _plan_objs(gen.complete(3), 10)
+    assert len(c) == 4 and c[0] == 0 and c[-1] == 3   # p clamped to n
+
+
+def test_cuts_balance_property():
+    # prefix cuts: every part's weight <= W/p + max single weight
+    g = gen.rmat(10, 16, 2)
+    for rule in (0, 1):
+        for p in (2, 3, 5, 8):
+            n, D, c = _plan_objs(g, p, rule)
+            w = np.array([int(x) for x in ob.cut_weights(n, D, rule)], dtype=np.int64)
+            assert (np.diff(c) >= 0).all()
+            parts = [w[c[k]:c[k + 1]].sum() for k in range(p)]
+            assert max(parts) <= w.sum() / p + w.max()
+
+
+# ---- S5 blocks -------------------------------------------------------------------
+def test_blocks_k3_hand():
+    # K3: rank = id; DAG (0,1),(0,2),(1,2); rule 0 w=[2,2,0] -> cuts [0,1,3]
+    # A_00 empty; A_01 row0 -> local cols {0,1}; A_11 row0 -> {1}
+    n, D, c = _plan_objs(gen.complete(3), 2)
+    assert list(c) == [0, 1, 3]
+    B = ob.blocks(D, c)
+    assert B[(0, 0)][1].size == 0
+    assert list(B[(0, 1)][0]) == [0, 2] and list(B[(0, 1)][1]) == [0, 1]
+    assert list(B[(1, 1)][0]) == [0, 1, 1] and list(B[(1, 1)][1]) == [1]
+
+
+def test_blocks_edge_cover():
+    g = gen.rmat(10, 16, 4)
+    for p in (1, 2, 3, 5, 8):
+        n, D, c = _plan_objs(g, p)
+        B = ob.blocks(D, c)
+        assert sum(v[1].size for v in B.values()) == len(D)
+        got = set()
+        for (i, j), (rp, col) in B.items():
+            for r in range(rp.size - 1):
+                for v in col[rp[r]:rp[r + 1]]:
+                    got.add((int(r + c[i]), int(v + c[j])))
+        assert got == {tuple(map(int, e)) for e in D}
+
+
+# ---- S6 tasks + S10 counts: the block method's correctness theorem ------------------
+def test_tasks_k3_hand_and_counts():
+    # tasks (0,1,1), (1,1,1); counts: edge (0->1) finds {2}; others 0 -> [1, 0]
+    P = ob.Plan(*gen.complete(3), p=2)
+    assert P.tasks == [(0, 1, 1), (1, 1, 1)]
+    assert P.task_counts() == [1, 0]
+
+
+def test_tasks_dense_is_all_triples():
+    P = ob.Plan(*gen.complete(40), p=4)
+    assert len(P.tasks) == comb(4 + 2, 3)
+
+
+def test_p4_tasks_hand():
+    P = ob.Plan(*gen.path(4), p=2)
+    assert P.tasks == [(0, 1, 1), (1, 1, 1)]
+    assert P.task_counts() == [0, 0]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8])
+def test_sum_task_counts_is_T(p):
+    for g in (gen.rmat(8, 16, 1), gen.er_small(120, 0.15, 3), gen.king(6, 7), gen.wheel(30)):
+        P = ob.Plan(*g, p=p)
+        tc = P.task_counts()
+        assert sum(tc) == oracle.count(*g) == oracle.brute(*g)
+
+
+def test_p1_single_task():
+    g = gen.rmat(8, 16, 5)
+    P = ob.Plan(*g, p=1)
+    assert P.tasks == [(0, 0, 0)]
+    assert P.task_counts() == [oracle.count(*g)]
+
+
+# ---- S7 cost and algorithmic bytes: hand examples ----------------------------------
+def test_cost_k4_hand():
+    # K4, p=1: d+ = [3,2,1,0]; cost = sum over DAG edges (d+(u)+d+(v))
+    #   = 5+4+3+3+2+1 = 18; alg elements = (3+2+1) + (2+1+0+1+0+0) = 10 -> 40 + 12*6
+    P = ob.Plan(*gen.complete(4), p=1)
+    assert P.costs == [18]
+    assert P.alg_bytes == [4 * 10 + 12 * 6]
+
+
+def test_cost_k3_p2_hand():
+    # (0,1,1): edges (0,0): 2+1, (0,1): 2+0 -> 5; (1,1,1): edge (0,1): 1+0 -> 1
+    # alg: (0,1,1): 2 + (1+0) = 3 el, 2 edges -> 36; (1,1,1): 1 + 0 el, 1 edge -> 16
+    P = ob.Plan(*gen.complete(3), p=2)
+    assert P.costs == [5, 1]
+    assert P.alg_bytes == [36, 16]
+
+
+# ---- S8 pieces and LPT -------------------------------------------------------------
+def test_pieces_k4_hand():
+    # G=2: cap = ceil(18/8) = 3, k = 6; row costs [12,5,1,0], R=[0,12,17,18,18]
+    # boundaries q=1..5 -> [1,1,1,1,2]; pieces [0,1):12, [1,2):5, [2,4):1
+    P = ob.Plan(*gen.complete(4), p=1, G=2)
+    assert P.pieces == [(0, 0, 1, 12), (0, 1, 2, 5), (0, 2, 4, 1)]
+    assert P.owner == [0, 1, 1]
+    assert P.loads == [12, 6]
+
+
+def test_lpt_hand():
+    pcs = [(0, 0, 1, 5), (1, 0, 1, 4), (2, 0, 1, 3), (3, 0, 1, 3), (4, 0, 1, 3)]
+    owner, loads = ob.lpt(pcs, 2)
+    assert owner == [0, 1, 1, 0, 1] and loads == [8, 10]
+
+
+def test_lpt_within_graham_bound():
+    rng = np.random.default_rng(1)
+    for _ in range(30):
+        G = int(rng.integers(2, 4))
+        costs = [int(x) for x in rng.integers(1, 50, size=int(rng.integers(3, 8)))]
+        pcs = [(k, 0, 1, c) for k, c in enumerate(costs)]
+        _, loads = ob.lpt(pcs, G)
+        opt = min(max(sum(c for c, a in zip(costs, asg) if a == g) for g in range(G))
+                  for asg in itertools.product(range(G), repeat=len(costs)))
+        assert max(loads) <= (4 / 3 - 1 / (3 * G)) * opt + 1e-9
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_pieces_partition_tasks(G):
+    g = gen.rmat(9, 16, 7)
+    P = ob.Plan(*g, p=3, G=G)
+    tc = P.task_counts()
+    for ti, t in enumerate(P.tasks):
+        mine = [pc for pc in P.pieces if pc[0] == ti]
+        assert sum(pc[3] for pc in mine) == P.costs[ti]
+        assert sum(ob.piece_count(P.B, t, pc[1], pc[2]) for pc in mine) == tc[ti]
+        for a, b in zip(mine, mine[1:]):
+            assert a[2] <= b[1]
+    per_rank = [0] * G
+    for pc, o in zip(P.pieces, P.owner):
+        per_rank[o] += ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2])
+    assert sum(per_rank) == oracle.count(*g)
