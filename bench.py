@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py -- triangle-count |E|/s of the block-based TC path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one pgabb_triangle_count over the whole graph (S9..S11: the block
+intersections of every task this rank owns, the count reduction and, for N>1,
+the 8-byte NCCL allreduce), with the block CSR already resident in HBM.  Build
+(S1..S8) is pre-processing, excluded as in the paper and
+reported separately.  `e2e` is the same metric through the same public call on
+a host-resident handle: every step copies the blocks host->device from pinned
+memory and reads the count back (the paper's own protocol).
+
+Rank 0 prints ONE JSON line.  See DESIGN.md §6 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "triangle-count edges/sec (|E|/time)"
+UNIT = "edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
+    ap.add_argument("--cut-rule", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            js = json.load(f)
+        return js.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg_name, n, s, d, target_s):
+    """The oracle (oracle/tc_oracle.c) as it stands, on this host's cores, over a
+    bounded vertex-stride sample of the same graph (full graph when it fits)."""
+    import oracle
+    t0 = time.perf_counter()
+    g = oracle.Graph(n, s, d)
+    t_build = time.perf_counter() - t0
+    # probe with a 1/256 stride sample, then size the sample to ~target_s
+    t0 = time.perf_counter()
+    _, e_probe = g.count_range(0, n, 256)
+    t_probe = max(time.perf_counter() - t0, 1e-4)
+    est_full = t_probe * 256
+    stride = 1 if est_full <= target_s else max(1, int(est_full / target_s + 0.999))
+    t0 = time.perf_counter()
+    T_s, e_s = g.count_range(0, n, stride)
+    dt = time.perf_counter() - t0
+    m_edges = g.m_edges
+    g.close()
+    sample = ("full graph" if stride == 1 else
+              f"every {stride}-th vertex as the lowest triangle vertex ({e_s} of {m_edges} DAG edges)")
+    return {"value": e_s / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"{cfg_name}: node iterator over {sample}; oracle build {t_build:.1f}s excluded",
+            "seconds": dt, "triangles_in_sample": T_s, "full": stride == 1}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from gen.configs import CONFIGS
+    import oracle
+    cfg = CONFIGS[args.config]
+    n, s, d = cfg.generate()
+    g = oracle.Graph(n, s, d)
+    m_edges = g.m_edges
+    t0 = time.perf_counter()
+    _, e_probe = g.count_range(0, n, 256)
+    t_probe = max(time.perf_counter() - t0, 1e-4)
+    per_step = max(1.0, 60.0 / max(args.steps + args.warmup, 1))   # whole run ~1 min
+    stride = max(1, int(t_probe * 256 / per_step + 0.999))
+    times, edges = [], []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, e = g.count_range(k % stride, n, stride)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+            edges.append(e)
+    g.close()
+    value = sum(edges) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "m_edges": m_edges,
+                   "sample_stride": stride},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+                         "sample": f"each step: node iterator over every {stride}-th vertex (rotating offset)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from gen.configs import CONFIGS
+    import paper_2209_04541_b200 as pg
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    cfg = CONFIGS[args.config]
+    p = args.p or cfg.p
+    n, s, d = cfg.generate()
+    m_tuples = int(s.size)
+
+    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
+    st0 = b.stats()
+    m_edges = int(st0["m_edges"])
+    stream = torch.cuda.current_stream()
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step():
+        b.triangle_count(stream=stream.cuda_stream, d_count=out.data_ptr(), sync=False)
+        if ws > 1:
+            dist.all_reduce(out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    T = int(out.item())
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms, launches = [], 0
+    with ClockSampler(dev) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (outside events)
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+            stk = b.stats()
+            kern_ms.append(stk["ms_main_kernel_last"])
+            launches += int(stk["launches_last"])
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    step_ms = [a.elapsed_time(z) for a, z in ev]
+    tot_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = m_edges / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (the intersection kernel, S10)
+    peak, peak_src = load_peaks()
+    st = b.stats()
+    alg = int(st["alg_bytes_local"])
+    kms = statistics.mean(kern_ms) if kern_ms else float("nan")
+    achieved = alg / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.config),
+                "kernel": "k_tc_warp (S10 intersections)", "kernel_ms": kms,
+                "kernel_share_of_step": kms / ms_per_step if ms_per_step else None,
+                "alg_bytes_per_launch": alg, "peak_source": peak_src}
+
+    # e2e: host-resident handle through the same public call, H2D inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+                             residency=pg.RESIDENT_HOST)
+        for _ in range(max(1, args.warmup)):
+            bh.triangle_count()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            local = bh.triangle_count()        # H2D of blocks + count + D2H of the count
+            if ws > 1:
+                tt = torch.tensor([local], dtype=torch.int64, device="cuda")
+                dist.all_reduce(tt)
+                tt.item()
+            wall.append(time.perf_counter() - t0)
+        e_s = sum(wall)
+        if ws > 1:
+            t = torch.tensor([e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_s = float(t.item())
+        sh = bh.stats()
+        e2e = {"value": m_edges / (e_s / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": int(sh["h2d_bytes_last"]), "d2h_bytes_per_step": 8,
+               "ms_per_step": 1e3 * e_s / args.steps}
+        bh.free()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg.name, n, s, d, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n, "tuples": m_tuples, "m_edges": m_edges,
+                       "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
+                       "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
+                       "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "timer": "CUDA events per step on the launch stream, max over ranks"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if cpu and cpu.get("full"):
+            line["parity"] = {"oracle_triangles": cpu["triangles_in_sample"],
+                              "match": cpu["triangles_in_sample"] == T}
+        print(json.dumps(line), flush=True)
+    b.free()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,174 @@
+/*
+ * pgabb.h -- C ABI of the B200-native block-based triangle counter
+ * (PGAbB, arXiv 2209.04541, the triangle-counting path of §3.6 / §5.4).
+ *
+ * The problem (§3.6 "An example: triangle counting"):
+ *   "find the number of mutually connected sets of three vertices in an
+ *    undirected graph".  Inputs are made "undirected, and removed duplicate
+ *    edges" (§5.1), so tuples may hold both directions,
+ *    duplicates and self-loops; the library canonicalises them (R1-R2).
+ *
+ * The method:
+ *   pgabb_build_blocks    S1 canonicalise, S2 degree order,
+ *                         S3 orient into a DAG ("only requires half of the
+ *                         edges"), S4 conformal p-way cuts
+ *                         (§4.3), S5 per-block CSR
+ *                         (§4.3.2), S6 block triples
+ *                         <A_ij, A_ix, A_jx> (Listing 5),
+ *                         S7 task costs (the E functor),
+ *                         S8 pieces + LPT over ranks.
+ *   pgabb_triangle_count  S9 residency (host->device copy for host-resident
+ *                         handles), S10 the intersections
+ *                         n_t += |A_ix[u] ∩ A_jx[v]| for every (u,v) in A_ij
+ *                         (Listing 5), S11 the count reduction.
+ *
+ * Conventions (all entry points):
+ *   - No C++ types or exceptions cross this boundary.  Every function returns a
+ *     pgabb_status_t; on a non-OK status the output arguments are left untouched
+ *     and pgabb_last_error() returns a thread-local message.
+ *   - Input buffers are BORROWED for the duration of the call only.
+ *   - A handle is owned by the library until pgabb_free(); one handle must not be
+ *     used from two threads at once.  Distinct handles are independent.
+ *   - All counts are exact uint64 and identical for every p, cut rule, world
+ *     size, residency and run (SPEC.md:468 invariance; R10).
+ *   - There is no CPU fallback: without a usable CUDA device (sm_100a) the calls
+ *     return PGABB_ECUDA.
+ */
+#ifndef PGABB_H
+#define PGABB_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PGABB_API __attribute__((visibility("default")))
+#else
+#define PGABB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pgabb_blocks_s* pgabb_blocks_t;
+
+typedef enum {
+    PGABB_OK = 0,
+    PGABB_EINVAL = 1,   /* bad argument: vertex id >= n, NULL pointer, bad option */
+    PGABB_ENOMEM = 2,   /* device or pinned-host allocation failed */
+    PGABB_ECUDA = 3,    /* CUDA error (incl. no device) */
+    PGABB_ERANGE = 4,   /* size outside the supported range (|E| >= 2^32, n >= 2^31) */
+    PGABB_EBUDGET = 5   /* host-resident handle: one task's 3 blocks exceed the budget */
+} pgabb_status_t;
+
+/* Residency of the block CSR (S9; §4.4). */
+enum {
+    PGABB_RESIDENT_DEVICE = 0,  /* blocks live in HBM; counting reads them in place */
+    PGABB_RESIDENT_HOST = 1     /* blocks live in pinned host DRAM; every count call
+                                   copies the blocks its tasks need host->device
+                                   (within device_budget_bytes) -- the paper's
+                                   protocol, where H2D is part of the timed count
+                                    */
+};
+
+typedef struct {
+    uint32_t p;                 /* parts per dimension; 0 = 8; clamped to [1, n] */
+    uint32_t cut_rule;          /* 0 = balance estimated work w(v) = d+(v) + d-(v)d+(v)
+                                   1 = balance DAG out-degree w(v) = d+(v)   (DESIGN R7) */
+    int32_t device;             /* CUDA ordinal, -1 = current device */
+    uint32_t inputs_on_device;  /* 1: src/dst are device pointers on `device` */
+    int32_t rank;               /* this handle's rank in [0, world_size) (S8) */
+    int32_t world_size;         /* ranks sharing the tasks; <= 1 means one GPU */
+    uint32_t residency;         /* PGABB_RESIDENT_DEVICE or PGABB_RESIDENT_HOST */
+    uint32_t reserved0;
+    uint64_t device_budget_bytes; /* HOST residency: device bytes for staged blocks;
+                                     0 = stage all of this rank's blocks at once */
+} pgabb_build_opts_t;
+
+/* Fills *opts with the defaults (p=0->8, rule 0, current device, one rank, HBM). */
+PGABB_API void pgabb_default_build_opts(pgabb_build_opts_t* opts);
+
+/*
+ * S1-S8.  n: number of vertex ids; m: number of tuples; src[k], dst[k] < n are
+ * the k-th tuple (uint32, host memory unless opts->inputs_on_device).  m == 0 is
+ * valid (an empty graph, count 0).  Requires n < 2^31 and |E| < 2^32.
+ * opts == NULL means defaults.  On success *out receives a new handle.
+ * Errors: EINVAL (id >= n, src/dst NULL with m > 0, out NULL, bad rank/p/rule),
+ *         ERANGE, ENOMEM, ECUDA.
+ */
+PGABB_API pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src,
+                                  const uint32_t* dst, const pgabb_build_opts_t* opts,
+                                  pgabb_blocks_t* out);
+
+typedef struct {
+    void* cuda_stream;          /* cudaStream_t to order the work on; NULL = handle's stream */
+    uint64_t* d_count;          /* optional DEVICE uint64*: receives this rank's count,
+                                   stream-ordered (for a caller-side NCCL allreduce) */
+    uint64_t* task_counts;      /* optional HOST uint64[ntasks]: per-task counts of the
+                                   pieces this rank owns (others 0) */
+    uint32_t flags;             /* PGABB_COUNT_ASYNC: do not wait; *triangles untouched */
+    uint32_t reserved0;
+} pgabb_count_opts_t;
+
+#define PGABB_COUNT_ASYNC 1u
+
+/*
+ * S9-S11.  Counts the triangles of the pieces this handle's rank owns (all of
+ * them when world_size <= 1) and writes the count to *triangles (host).  The
+ * sum over ranks 0..world_size-1 of their counts is the triangle count T of the
+ * canonicalised graph; combining them is the caller's allreduce (the Python
+ * binding issues one NCCL allreduce of 8 bytes through torch.distributed).
+ * opts == NULL: handle's stream, synchronous.
+ */
+PGABB_API pgabb_status_t pgabb_triangle_count(pgabb_blocks_t b, const pgabb_count_opts_t* opts,
+                                    uint64_t* triangles);
+
+typedef struct {
+    uint64_t n, m_tuples, m_edges;      /* m_edges = |E| = |E+| (DESIGN R15) */
+    uint64_t p, ntasks, npieces, npieces_local;
+    uint64_t wedges;                    /* W = sum_v d-(v) d+(v) */
+    uint64_t cost_total, cost_local;    /* S7 cost units (DESIGN R17) */
+    uint64_t alg_bytes_total, alg_bytes_local; /* staged-model bytes (R19) */
+    uint64_t block_bytes;               /* bytes of block CSR (all blocks) */
+    uint64_t h2d_bytes_last;            /* host->device bytes of the last count call */
+    uint64_t launches_last;             /* kernels launched by the last count call */
+    uint64_t reserved[4];
+    double ms_build;                    /* wall time of pgabb_build_blocks */
+    double ms_count_last;               /* device time of the last count call (events) */
+    double ms_main_kernel_last;         /* device time of the intersection kernels */
+    double reserved_d[3];
+} pgabb_stats_t;
+
+PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);
+
+/* ---- introspection (parity tests of S2..S8); all outputs are HOST buffers ---- */
+
+/* rank[v] for every original id v < n: the position of v in the (deg, id) order. */
+PGABB_API pgabb_status_t pgabb_get_rank(pgabb_blocks_t b, uint32_t* rank);
+/* cuts[0..p] (rank space). */
+PGABB_API pgabb_status_t pgabb_get_cuts(pgabb_blocks_t b, uint32_t* cuts);
+/* Block A_ij, i <= j < p: *nnz always; rowptr[0..cut_{i+1}-cut_i] and col[0..nnz)
+ * (local ids) when non-NULL.  EINVAL for i > j or j >= p. */
+PGABB_API pgabb_status_t pgabb_get_block(pgabb_blocks_t b, uint32_t i, uint32_t j, uint32_t* rowptr,
+                               uint32_t* col, uint64_t* nnz);
+/* Tasks in (i, j, x) lexicographic order: ijx[3*t..3*t+2], cost[t], alg_bytes[t];
+ * any output may be NULL. */
+PGABB_API pgabb_status_t pgabb_get_tasks(pgabb_blocks_t b, uint32_t* ijx, uint64_t* cost,
+                               uint64_t* alg_bytes);
+/* Pieces (S8) in (task, row) order: task[k], row_begin[k], row_end[k] (local rows of
+ * part i), cost[k], owner[k] (rank); any output may be NULL. */
+PGABB_API pgabb_status_t pgabb_get_pieces(pgabb_blocks_t b, uint32_t* task, uint32_t* row_begin,
+                                uint32_t* row_end, uint64_t* cost, int32_t* owner);
+
+/* Frees device and pinned-host memory.  NULL is a no-op. */
+PGABB_API void pgabb_free(pgabb_blocks_t b);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+PGABB_API const char* pgabb_last_error(void);
+
+/* Library version string. */
+PGABB_API const char* pgabb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGABB_H */

@@ -1,0 +1,190 @@
+"""B200-native block-based triangle counting (PGAbB, arXiv 2209.04541, §3.6 / §5.4).
+
+Thin Python binding over the C ABI in ``include/pgabb.h`` (``libpgabb.so``):
+argument marshalling only -- every step of the path (S1..S11)
+runs in the CUDA library.  There is no CPU fallback: importing this package
+without the built library raises ImportError, and calls without a CUDA device
+raise :class:`PgabbError` (ECUDA).
+
+    import paper_2209_04541_b200 as pg
+    with pg.build_blocks(n, src, dst, p=8) as b:     # S1..S8
+        T = b.triangle_count()                          # S9..S11
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _abi
+
+_lib = _abi.load()
+
+RESIDENT_DEVICE = _abi.RESIDENT_DEVICE
+RESIDENT_HOST = _abi.RESIDENT_HOST
+
+
+class PgabbError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.pgabb_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_abi.STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = _abi.STATUS.get(status, str(status))
+
+
+def _ck(st: int, where: str):
+    if st != 0:
+        raise PgabbError(st, where)
+
+
+def version() -> str:
+    return _lib.pgabb_version().decode()
+
+
+def _pointer(x):
+    """(pointer, length, on_device, keepalive) for a numpy array or torch tensor of uint32/int32."""
+    if hasattr(x, "data_ptr") and hasattr(x, "is_cuda"):
+        import torch
+        if x.dtype not in (torch.int32, torch.uint32):
+            raise TypeError("tuples must be 32-bit integers")
+        x = x.contiguous()
+        if x.is_cuda:
+            return x.data_ptr(), x.numel(), True, x
+        x = x.numpy()
+    a = np.ascontiguousarray(x)
+    if a.dtype not in (np.uint32, np.int32):
+        a = a.astype(np.uint32)
+    return a.ctypes.data, a.size, False, a
+
+
+class Blocks:
+    """A built block grid (handle).  Use as a context manager or call free()."""
+
+    def __init__(self, handle, ntasks: int, p: int, n: int):
+        self._h = handle
+        self.ntasks = ntasks
+        self.p = p
+        self.n = n
+
+    # --- lifetime ---
+    def free(self):
+        if self._h:
+            _lib.pgabb_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.free()
+
+    # --- S9..S11 ---
+    def triangle_count(self, stream=None, d_count=None, task_counts: bool = False, sync: bool = True):
+        """This rank's triangle count (host int).  stream: a cudaStream_t int or torch
+        stream; d_count: device pointer (int) receiving the count; task_counts: also
+        return the per-task counts."""
+        o = _abi.CountOpts()
+        if stream is not None:
+            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+        if d_count is not None:
+            o.d_count = d_count
+        tc = np.zeros(max(self.ntasks, 1), np.uint64) if task_counts else None
+        if tc is not None:
+            o.task_counts = tc.ctypes.data_as(_abi.u64p)
+        if not sync:
+            o.flags = _abi.COUNT_ASYNC
+        out = ctypes.c_uint64(0)
+        _ck(_lib.pgabb_triangle_count(self._h, ctypes.byref(o), ctypes.byref(out)), "pgabb_triangle_count")
+        if not sync:
+            return None
+        return (int(out.value), tc[:self.ntasks]) if task_counts else int(out.value)
+
+    # --- introspection ---
+    def stats(self) -> dict:
+        s = _abi.Stats()
+        _ck(_lib.pgabb_get_stats(self._h, ctypes.byref(s)), "pgabb_get_stats")
+        return s.as_dict()
+
+    def rank(self) -> np.ndarray:
+        out = np.empty(max(self.n, 1), np.uint32)
+        _ck(_lib.pgabb_get_rank(self._h, out.ctypes.data_as(_abi.u32p)), "pgabb_get_rank")
+        return out[:self.n]
+
+    def cuts(self) -> np.ndarray:
+        out = np.empty(self.p + 1, np.uint32)
+        _ck(_lib.pgabb_get_cuts(self._h, out.ctypes.data_as(_abi.u32p)), "pgabb_get_cuts")
+        return out
+
+    def block(self, i: int, j: int):
+        """(rowptr, col) of A_ij, local ids."""
+        nnz = ctypes.c_uint64(0)
+        _ck(_lib.pgabb_get_block(self._h, i, j, None, None, ctypes.byref(nnz)), "pgabb_get_block")
+        c = self.cuts()
+        rp = np.empty(int(c[i + 1] - c[i]) + 1, np.uint32)
+        col = np.empty(max(int(nnz.value), 1), np.uint32)
+        _ck(_lib.pgabb_get_block(self._h, i, j, rp.ctypes.data_as(_abi.u32p), col.ctypes.data_as(_abi.u32p),
+                                 ctypes.byref(nnz)), "pgabb_get_block")
+        return rp, col[:int(nnz.value)]
+
+    def tasks(self):
+        """(ijx[ntasks,3], cost[ntasks], alg_bytes[ntasks])."""
+        nt = max(self.ntasks, 1)
+        ijx = np.empty(3 * nt, np.uint32)
+        cost = np.empty(nt, np.uint64)
+        alg = np.empty(nt, np.uint64)
+        _ck(_lib.pgabb_get_tasks(self._h, ijx.ctypes.data_as(_abi.u32p), cost.ctypes.data_as(_abi.u64p),
+                                 alg.ctypes.data_as(_abi.u64p)), "pgabb_get_tasks")
+        k = self.ntasks
+        return ijx[:3 * k].reshape(k, 3), cost[:k], alg[:k]
+
+    def pieces(self):
+        """list of (task, row_begin, row_end, cost) and owner list."""
+        npc = int(self.stats()["npieces"])
+        m = max(npc, 1)
+        t, r0, r1 = (np.empty(m, np.uint32) for _ in range(3))
+        c = np.empty(m, np.uint64)
+        o = np.empty(m, np.int32)
+        _ck(_lib.pgabb_get_pieces(self._h, t.ctypes.data_as(_abi.u32p), r0.ctypes.data_as(_abi.u32p),
+                                  r1.ctypes.data_as(_abi.u32p), c.ctypes.data_as(_abi.u64p),
+                                  o.ctypes.data_as(_abi.i32p)), "pgabb_get_pieces")
+        pcs = [(int(t[k]), int(r0[k]), int(r1[k]), int(c[k])) for k in range(npc)]
+        return pcs, [int(o[k]) for k in range(npc)]
+
+
+def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = -1, rank: int = 0,
+                 world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0) -> Blocks:
+    """S1..S8: canonicalise, degree-order, orient, cut, block, enumerate, cost, assign.
+
+    src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device)."""
+    sp, sn, sdev, keep_s = _pointer(src)
+    dp, dn, ddev, keep_d = _pointer(dst)
+    if sn != dn:
+        raise ValueError("src and dst differ in length")
+    if sdev != ddev:
+        raise ValueError("src and dst must both be host or both be device arrays")
+    o = _abi.BuildOpts()
+    _lib.pgabb_default_build_opts(ctypes.byref(o))
+    o.p, o.cut_rule, o.device = p, cut_rule, device
+    o.inputs_on_device = int(sdev)
+    o.rank, o.world_size, o.residency = rank, world_size, residency
+    o.device_budget_bytes = device_budget_bytes
+    h = ctypes.c_void_p(0)
+    st = _lib.pgabb_build_blocks(int(n), int(sn), ctypes.c_void_p(sp) if sn else None,
+                                 ctypes.c_void_p(dp) if dn else None, ctypes.byref(o), ctypes.byref(h))
+    del keep_s, keep_d
+    _ck(st, "pgabb_build_blocks")
+    s = _abi.Stats()
+    _ck(_lib.pgabb_get_stats(h, ctypes.byref(s)), "pgabb_get_stats")
+    return Blocks(h, int(s.ntasks), int(s.p), int(n))
+
+
+def triangle_count(n: int, src, dst, **kw) -> int:
+    """One-shot convenience: build, count, free."""
+    with build_blocks(n, src, dst, **kw) as b:
+        return b.triangle_count()

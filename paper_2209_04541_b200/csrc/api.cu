@@ -1,0 +1,255 @@
+// api.cu -- the C ABI of include/pgabb.h: argument checking, handle lifetime,
+// exception -> status translation, introspection copies.
+#include <chrono>
+#include <cstring>
+
+#include "internal.h"
+
+namespace pgabb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void fail(pgabb_status_t st, const std::string& msg) { throw Error{st, msg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    (void)cudaGetLastError();
+    const pgabb_status_t st = (e == cudaErrorMemoryAllocation) ? PGABB_ENOMEM : PGABB_ECUDA;
+    fail(st, std::string(what) + " -> " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e) + " (" + file +
+                 ":" + std::to_string(line) + ")");
+}
+
+template <class F>
+pgabb_status_t guarded(F f) {
+    try {
+        f();
+        g_last_error.clear();
+        return PGABB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return PGABB_ENOMEM;
+    } catch (...) {
+        g_last_error = "unexpected internal error";
+        return PGABB_ECUDA;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0) PG_CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace pgabb
+
+pgabb_blocks_s::~pgabb_blocks_s() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    d_rank.release();
+    d_col.release();
+    d_rowptr.release();
+    d_work.release();
+    d_task_counts.release();
+    d_next.release();
+    h_col.release();
+    h_rowptr.release();
+    h_result.release();
+    for (cudaEvent_t e : {ev0, ev1, ev2, ev3})
+        if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+using namespace pgabb;
+
+extern "C" {
+
+void pgabb_default_build_opts(pgabb_build_opts_t* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->p = 0;
+    o->cut_rule = 0;
+    o->device = -1;
+    o->inputs_on_device = 0;
+    o->rank = 0;
+    o->world_size = 1;
+    o->residency = PGABB_RESIDENT_DEVICE;
+    o->device_budget_bytes = 0;
+}
+
+pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                                  const pgabb_build_opts_t* opts_in, pgabb_blocks_t* out) {
+    pgabb_blocks_s* h = nullptr;
+    pgabb_status_t st = guarded([&] {
+        if (!out) fail(PGABB_EINVAL, "out is NULL");
+        if (m > 0 && (!src || !dst)) fail(PGABB_EINVAL, "src/dst NULL with m > 0");
+        if (n >= (1u << 31)) fail(PGABB_ERANGE, "n >= 2^31 is not supported");
+        pgabb_build_opts_t o;
+        pgabb_default_build_opts(&o);
+        if (opts_in) o = *opts_in;
+        if (o.cut_rule > 1) fail(PGABB_EINVAL, "cut_rule must be 0 or 1");
+        if (o.residency > PGABB_RESIDENT_HOST) fail(PGABB_EINVAL, "bad residency");
+        if (o.world_size < 1) o.world_size = 1;
+        if (o.rank < 0 || o.rank >= o.world_size) fail(PGABB_EINVAL, "rank outside [0, world_size)");
+        if (o.p > (uint32_t)kMaxParts) fail(PGABB_EINVAL, "p > 64 is not supported");
+        const auto t0 = std::chrono::steady_clock::now();
+        int dev = o.device;
+        if (dev < 0) PG_CK(cudaGetDevice(&dev));
+        int ndev = 0;
+        PG_CK(cudaGetDeviceCount(&ndev));
+        if (dev >= ndev) fail(PGABB_EINVAL, "device ordinal out of range");
+        DeviceGuard g(dev);
+        h = new pgabb_blocks_s();
+        h->device = dev;
+        PG_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&h->ev0, &h->ev1, &h->ev2, &h->ev3}) PG_CK(cudaEventCreate(e));
+        h->h_result.alloc(1);
+        h->n = n;
+        h->m_tuples = m;
+        uint32_t p = o.p ? o.p : 8;
+        p = (n > 0) ? std::max<uint32_t>(1, std::min<uint32_t>(p, n)) : 1;   // DESIGN R7
+        h->p = p;
+        h->cut_rule = o.cut_rule;
+        h->rank = o.rank;
+        h->world_size = o.world_size;
+        h->residency = o.residency;
+        h->budget = o.device_budget_bytes;
+        build_graph(h, m, src, dst, o.inputs_on_device != 0);
+        plan_pieces(h);
+        upload_work(h);
+        if (h->residency == PGABB_RESIDENT_HOST) {
+            h->h_col.alloc(h->d_col.n);
+            h->h_rowptr.alloc(h->d_rowptr.n);
+            if (h->d_col.n) PG_CK(cudaMemcpy(h->h_col.p, h->d_col.p, h->d_col.bytes(), cudaMemcpyDeviceToHost));
+            if (h->d_rowptr.n)
+                PG_CK(cudaMemcpy(h->h_rowptr.p, h->d_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyDeviceToHost));
+        }
+        PG_CK(cudaStreamSynchronize(h->stream));
+        h->ms_build = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        *out = h;
+    });
+    if (st != PGABB_OK && h) delete h;
+    return st;
+}
+
+pgabb_status_t pgabb_triangle_count(pgabb_blocks_t b, const pgabb_count_opts_t* opts, uint64_t* triangles) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "handle is NULL");
+        const bool async = opts && (opts->flags & PGABB_COUNT_ASYNC);
+        if (!triangles && !async) fail(PGABB_EINVAL, "triangles is NULL");
+        DeviceGuard g(b->device);
+        bool wrote = false;
+        const uint64_t T = count_triangles(b, opts, &wrote);
+        if (wrote) *triangles = T;
+    });
+}
+
+pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
+    return guarded([&] {
+        if (!b || !s) fail(PGABB_EINVAL, "NULL argument");
+        if (b->timing_pending) {
+            DeviceGuard g(b->device);
+            resolve_timing(b);
+        }
+        std::memset(s, 0, sizeof(*s));
+        s->n = b->n;
+        s->m_tuples = b->m_tuples;
+        s->m_edges = b->m_edges;
+        s->p = b->p;
+        s->ntasks = b->tasks.size();
+        s->npieces = b->pieces.size();
+        s->npieces_local = b->work.size();
+        s->wedges = b->wedges;
+        s->cost_total = b->cost_total;
+        s->cost_local = b->cost_local;
+        s->alg_bytes_total = b->alg_total;
+        s->alg_bytes_local = b->alg_local;
+        s->block_bytes = b->d_col.bytes() + b->d_rowptr.bytes();
+        s->h2d_bytes_last = b->h2d_last;
+        s->launches_last = b->launches_last;
+        s->ms_build = b->ms_build;
+        s->ms_count_last = b->ms_count_last;
+        s->ms_main_kernel_last = b->ms_main_last;
+    });
+}
+
+pgabb_status_t pgabb_get_rank(pgabb_blocks_t b, uint32_t* rank) {
+    return guarded([&] {
+        if (!b || !rank) fail(PGABB_EINVAL, "NULL argument");
+        DeviceGuard g(b->device);
+        if (b->n) PG_CK(cudaMemcpy(rank, b->d_rank.p, (size_t)b->n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+pgabb_status_t pgabb_get_cuts(pgabb_blocks_t b, uint32_t* cuts) {
+    return guarded([&] {
+        if (!b || !cuts) fail(PGABB_EINVAL, "NULL argument");
+        std::memcpy(cuts, b->cuts.data(), b->cuts.size() * 4);
+    });
+}
+
+pgabb_status_t pgabb_get_block(pgabb_blocks_t b, uint32_t i, uint32_t j, uint32_t* rowptr, uint32_t* col,
+                               uint64_t* nnz) {
+    return guarded([&] {
+        if (!b || !nnz) fail(PGABB_EINVAL, "NULL argument");
+        if (i > j || j >= b->p) fail(PGABB_EINVAL, "block index must satisfy i <= j < p");
+        DeviceGuard g(b->device);
+        const BlockInfo& bi = b->blocks[(size_t)i * b->p + j];
+        *nnz = bi.nnz;
+        if (rowptr) {
+            if (bi.present)
+                PG_CK(cudaMemcpy(rowptr, b->d_rowptr.p + bi.rp_off, ((size_t)bi.nrows + 1) * 4, cudaMemcpyDeviceToHost));
+            else
+                std::memset(rowptr, 0, ((size_t)bi.nrows + 1) * 4);
+        }
+        if (col && bi.nnz)
+            PG_CK(cudaMemcpy(col, b->d_col.p + bi.col_off, bi.nnz * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+pgabb_status_t pgabb_get_tasks(pgabb_blocks_t b, uint32_t* ijx, uint64_t* cost, uint64_t* alg) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "NULL argument");
+        for (size_t t = 0; t < b->tasks.size(); ++t) {
+            const Task& T = b->tasks[t];
+            if (ijx) { ijx[3 * t] = T.i; ijx[3 * t + 1] = T.j; ijx[3 * t + 2] = T.x; }
+            if (cost) cost[t] = T.cost;
+            if (alg) alg[t] = T.alg_bytes;
+        }
+    });
+}
+
+pgabb_status_t pgabb_get_pieces(pgabb_blocks_t b, uint32_t* task, uint32_t* r0, uint32_t* r1, uint64_t* cost,
+                                int32_t* owner) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "NULL argument");
+        for (size_t k = 0; k < b->pieces.size(); ++k) {
+            const Piece& P = b->pieces[k];
+            if (task) task[k] = P.task;
+            if (r0) r0[k] = P.r0;
+            if (r1) r1[k] = P.r1;
+            if (cost) cost[k] = P.cost;
+            if (owner) owner[k] = P.owner;
+        }
+    });
+}
+
+void pgabb_free(pgabb_blocks_t b) { delete b; }
+
+const char* pgabb_last_error(void) { return g_last_error.c_str(); }
+
+const char* pgabb_version(void) { return "pgabb-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

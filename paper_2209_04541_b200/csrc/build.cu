@@ -1,0 +1,666 @@
+// build.cu -- S1..S8 of the block-based triangle-counting path on the GPU.
+//
+//   S1 canonicalise   (§5.1; DESIGN R1, R2)
+//   S2 degree order   (§5.4; DESIGN R3)
+//   S3 orient         (§5.4; DESIGN R4)
+//   S4 conformal cuts (§4.3; DESIGN R7)
+//   S5 block CSR      (§4.3.1-4.3.2)
+//   S6 block triples  (Listing 5; DESIGN R5, R6)
+//   S7 task costs     (§4.4; DESIGN R17, R19)
+//   S8 pieces + LPT   (§4.1; DESIGN R18)
+//
+// Pre-processing is untimed in the paper's protocol, but it
+// runs on the device anyway: 64-bit radix sorts of up to 2^31 keys (C5) are
+// far too slow on the host.  All arithmetic is integer.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <numeric>
+#include <queue>
+
+#include "internal.h"
+
+namespace pgabb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t work, int threads = kThreads) {
+    uint64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > (1u << 20)) g = 1u << 20;   // grid-stride beyond this
+    return (unsigned)g;
+}
+
+inline int bits_for(uint64_t x) {
+    int b = 0;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b;
+}
+
+struct CutsArg {
+    uint32_t c[kMaxParts + 1];
+    int p;
+};
+
+__device__ __forceinline__ int part_of(const CutsArg& cu, uint32_t r) {
+    // the j with cut_j <= r < cut_{j+1}: (number of cuts <= r) - 1
+    int lo = 0, hi = cu.p + 1;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (cu.c[mid] <= r) lo = mid + 1; else hi = mid;
+    }
+    return lo - 1;
+}
+
+__global__ void k_check_ids(const uint32_t* s, const uint32_t* d, uint64_t m, uint32_t n, int* bad) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        if (s[k] >= n || d[k] >= n) *bad = 1;
+}
+
+// S1: key = (min << B) | max, self-loops -> sentinel (all ones in 2B bits, never a
+// real key because a real key has min < max).
+__global__ void k_make_keys(const uint32_t* s, const uint32_t* d, uint64_t m, int B, uint64_t sent,
+                            uint64_t* keys) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a = s[k], b = d[k];
+        uint32_t lo = min(a, b), hi = max(a, b);
+        keys[k] = (a == b) ? sent : (((uint64_t)lo << B) | hi);
+    }
+}
+
+// S2: degree of every id over the unique undirected edges.
+__global__ void k_degree(const uint64_t* keys, uint64_t mE, int B, uint32_t* deg) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = keys[k];
+        atomicAdd(&deg[key >> B], 1u);
+        atomicAdd(&deg[key & mask], 1u);
+    }
+}
+
+__global__ void k_iota(uint32_t* a, uint32_t n) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        a[k] = (uint32_t)k;
+}
+
+__global__ void k_scatter_rank(const uint32_t* order, uint32_t n, uint32_t* rank) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        rank[order[k]] = (uint32_t)k;
+}
+
+// S3: relabel to rank space and orient low -> high.
+__global__ void k_orient(uint64_t* keys, uint64_t mE, int B, const uint32_t* rank) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = keys[k];
+        uint32_t ra = rank[key >> B], rb = rank[key & mask];
+        keys[k] = ((uint64_t)min(ra, rb) << B) | max(ra, rb);
+    }
+}
+
+__global__ void k_dag_degrees(const uint64_t* dag, uint64_t mE, int B, uint32_t* dplus, uint32_t* dminus) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = dag[k];
+        atomicAdd(&dplus[key >> B], 1u);
+        atomicAdd(&dminus[key & mask], 1u);
+    }
+}
+
+// S4 weights: rule 0 w = d+ + d- * d+, rule 1 w = d+; also wedges d- * d+.
+__global__ void k_cut_weights(const uint32_t* dplus, const uint32_t* dminus, uint32_t n, int rule,
+                              unsigned long long* w, unsigned long long* wedges) {
+    unsigned long long acc = 0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long dp = dplus[k], dm = dminus[k];
+        w[k] = rule == 0 ? dp + dm * dp : dp;
+        acc += dm * dp;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(wedges, acc);
+}
+
+// cut_j = min { c in [0, n] : p * P[c] >= j * P[n] },  P[0] = 0 (prefix of w).
+__global__ void k_cuts(const unsigned long long* P, uint32_t n, int p, uint32_t* cuts) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > p) return;
+    if (j == 0) { cuts[0] = 0; return; }
+    if (j == p) { cuts[p] = n; return; }
+    const unsigned __int128 tgt = (unsigned __int128)j * P[n];
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = lo + ((hi - lo) >> 1);
+        if ((unsigned __int128)p * P[mid] >= tgt) hi = mid; else lo = mid + 1;
+    }
+    cuts[j] = lo;
+}
+
+// S5: block id of each DAG edge.
+__global__ void k_block_ids(const uint64_t* dag, uint64_t mE, int B, CutsArg cu, uint32_t* bid) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = dag[k];
+        int i = part_of(cu, (uint32_t)(key >> B));
+        int j = part_of(cu, (uint32_t)(key & mask));
+        bid[k] = (uint32_t)(i * cu.p + j);
+    }
+}
+
+// off[b] = first position of block b in the block-sorted edge array.
+__global__ void k_block_offsets(const uint32_t* bid, uint64_t mE, uint32_t nb, unsigned long long* off) {
+    uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    uint64_t lo = 0, hi = mE;
+    while (lo < hi) {
+        uint64_t mid = lo + ((hi - lo) >> 1);
+        if (bid[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    off[b] = lo;
+}
+
+// col pool: local col id (c - cut_j) in block-major order.
+__global__ void k_local_cols(const uint64_t* dag, const uint32_t* bid, uint64_t mE, int B, CutsArg cu,
+                             uint32_t* col) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t j = bid[k] % cu.p;
+        col[k] = (uint32_t)(dag[k] & mask) - cu.c[j];
+    }
+}
+
+struct BlockDev {
+    unsigned long long col_off, nnz, rp_off;
+    uint32_t nrows, row_base;   // row_base = cut_i
+};
+
+// rowptr pool: for entry t of block b, rowptr[t] = #edges of b with local row < lr.
+__global__ void k_rowptr(const uint64_t* dag, int B, const BlockDev* blk, const unsigned long long* rp_start,
+                         int nblk, unsigned long long total, uint32_t* rowptr) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nblk;   // last block with rp_start <= t
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (rp_start[mid] <= t) lo = mid; else hi = mid;
+        }
+        const BlockDev bd = blk[lo];
+        const uint32_t lr = (uint32_t)(t - rp_start[lo]);
+        const uint64_t target = (uint64_t)bd.row_base + lr;   // global row
+        uint64_t a = 0, z = bd.nnz;
+        const uint64_t* e = dag + bd.col_off;
+        while (a < z) {
+            uint64_t mid = a + ((z - a) >> 1);
+            if ((e[mid] >> B) < target) a = mid + 1; else z = mid;
+        }
+        rowptr[t] = (uint32_t)a;
+    }
+}
+
+// S7: per-task cost and staged-model elements, one thread per edge of a
+// non-empty block; the x-loop visits every task (i,j,x) of the edge's block.
+struct CostArg {
+    const uint64_t* dag;
+    const uint32_t* col;
+    const uint32_t* rowptr;
+    const BlockDev* blk;          // indexed by block id i*p+j
+    const uint32_t* tid;          // p^3
+    int B, p;
+    CutsArg cu;
+    unsigned long long mE;
+    unsigned long long* cost;
+    unsigned long long* alg_el;
+};
+
+__global__ void k_task_costs(CostArg a) {
+    const uint64_t mask = (1ull << a.B) - 1;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < a.mE; k += stride) {
+        const uint64_t key = a.dag[k];
+        const uint32_t r = (uint32_t)(key >> a.B), c = (uint32_t)(key & mask);
+        const int i = part_of(a.cu, r), j = part_of(a.cu, c);
+        const uint32_t u = r - a.cu.c[i], v = c - a.cu.c[j];
+        const BlockDev bij = a.blk[i * a.p + j];
+        const bool first = (k == bij.col_off) || ((a.dag[k - 1] >> a.B) != r);
+        for (int x = j; x < a.p; ++x) {
+            const uint32_t t = a.tid[(i * a.p + j) * a.p + x];
+            if (t == kNoTask) continue;
+            const BlockDev bix = a.blk[i * a.p + x], bjx = a.blk[j * a.p + x];
+            const uint32_t la = a.rowptr[bix.rp_off + u + 1] - a.rowptr[bix.rp_off + u];
+            const uint32_t lb = a.rowptr[bjx.rp_off + v + 1] - a.rowptr[bjx.rp_off + v];
+            atomicAdd(&a.cost[t], (unsigned long long)(la + lb));
+            atomicAdd(&a.alg_el[t], (unsigned long long)(lb + (first ? la : 0u)));
+        }
+    }
+}
+
+// S8 helper: row costs of one task (for splitting heavy tasks into pieces).
+__global__ void k_row_costs(const uint32_t* col, const uint32_t* rowptr, BlockDev bij, BlockDev bix,
+                            BlockDev bjx, unsigned long long* rc) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < bij.nrows;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e0 = rowptr[bij.rp_off + u], e1 = rowptr[bij.rp_off + u + 1];
+        const uint32_t la = rowptr[bix.rp_off + u + 1] - rowptr[bix.rp_off + u];
+        unsigned long long s = 0;
+        for (uint32_t e = e0; e < e1; ++e) {
+            const uint32_t v = col[bij.col_off + e];
+            s += la + (rowptr[bjx.rp_off + v + 1] - rowptr[bjx.rp_off + v]);
+        }
+        rc[u + 1] = s;
+    }
+}
+
+template <class F>
+void cub_call(F f, cudaStream_t st, DBuf<unsigned char>& tmp) {
+    size_t bytes = 0;
+    PG_CK(f(nullptr, bytes));
+    if (bytes > tmp.bytes()) tmp.alloc(bytes);
+    PG_CK(f(tmp.p, bytes));
+    (void)st;
+}
+
+BlockDev to_dev(const BlockInfo& b, uint32_t row_base) {
+    BlockDev d;
+    d.col_off = b.col_off;
+    d.nnz = b.nnz;
+    d.rp_off = b.rp_off;
+    d.nrows = b.nrows;
+    d.row_base = row_base;
+    return d;
+}
+
+}  // namespace
+
+void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint32_t* dst, bool on_device) {
+    cudaStream_t st = h->stream;
+    const uint32_t n = h->n;
+    const int B = std::max(1, bits_for(n > 0 ? n - 1 : 0));
+    const uint64_t sent = (B >= 32) ? ~0ull : ((1ull << (2 * B)) - 1);
+    DBuf<unsigned char> tmp;
+
+    h->d_rank.alloc(std::max<uint32_t>(n, 1));
+    if (m == 0 || n == 0) {
+        h->m_edges = 0;
+        h->p = 1;
+        h->cuts = {0, n};
+        h->blocks.assign(1, BlockInfo{});
+        h->blocks[0].nrows = n;
+        if (n) {
+            k_iota<<<grid_for(n), kThreads, 0, st>>>(h->d_rank.p, n);
+            PG_LAUNCH_CHECK();
+        }
+        PG_CK(cudaStreamSynchronize(st));
+        return;
+    }
+
+    // ---- upload + validate --------------------------------------------------
+    DBuf<uint32_t> d_s, d_d;
+    const uint32_t *s = src, *d = dst;
+    if (!on_device) {
+        d_s.alloc(m);
+        d_d.alloc(m);
+        PG_CK(cudaMemcpyAsync(d_s.p, src, m * 4, cudaMemcpyHostToDevice, st));
+        PG_CK(cudaMemcpyAsync(d_d.p, dst, m * 4, cudaMemcpyHostToDevice, st));
+        s = d_s.p;
+        d = d_d.p;
+    }
+    DBuf<int> d_bad;
+    d_bad.alloc(1);
+    PG_CK(cudaMemsetAsync(d_bad.p, 0, 4, st));
+    k_check_ids<<<grid_for(m), kThreads, 0, st>>>(s, d, m, n, d_bad.p);
+    PG_LAUNCH_CHECK();
+    int bad = 0;
+    PG_CK(cudaMemcpyAsync(&bad, d_bad.p, 4, cudaMemcpyDeviceToHost, st));
+    PG_CK(cudaStreamSynchronize(st));
+    if (bad) fail(PGABB_EINVAL, "vertex id >= n in the input tuples");
+
+    // ---- S1 canonicalise ----------------------------------------------------
+    DBuf<uint64_t> keys, keys2;
+    keys.alloc(m);
+    keys2.alloc(m);
+    k_make_keys<<<grid_for(m), kThreads, 0, st>>>(s, d, m, B, sent, keys.p);
+    PG_LAUNCH_CHECK();
+    d_s.release();
+    d_d.release();
+    const int kbits = std::min(64, 2 * B);
+    cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, (int64_t)m, 0, kbits, st);
+    }, st, tmp);
+    DBuf<unsigned long long> d_cnt;
+    d_cnt.alloc(2);
+    cub_call([&](void* t, size_t& b) {
+        return cub::DeviceSelect::Unique(t, b, keys2.p, keys.p, d_cnt.p, (int64_t)m, st);
+    }, st, tmp);
+    unsigned long long nuniq = 0;
+    PG_CK(cudaMemcpyAsync(&nuniq, d_cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    PG_CK(cudaStreamSynchronize(st));
+    uint64_t mE = nuniq;
+    if (mE) {
+        uint64_t last = 0;
+        PG_CK(cudaMemcpy(&last, keys.p + (mE - 1), 8, cudaMemcpyDeviceToHost));
+        if (last == sent) --mE;
+    }
+    if (mE >= (1ull << 32)) fail(PGABB_ERANGE, "|E| >= 2^32 is not supported");
+    h->m_edges = mE;
+    keys2.release();
+
+    // ---- S2 degree + rank ---------------------------------------------------
+    {
+        DBuf<uint32_t> deg, deg2, ids, order;
+        deg.alloc(n);
+        deg2.alloc(n);
+        ids.alloc(n);
+        order.alloc(n);
+        PG_CK(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
+        if (mE) {
+            k_degree<<<grid_for(mE), kThreads, 0, st>>>(keys.p, mE, B, deg.p);
+            PG_LAUNCH_CHECK();
+        }
+        k_iota<<<grid_for(n), kThreads, 0, st>>>(ids.p, n);
+        PG_LAUNCH_CHECK();
+        // stable radix sort by degree: ties keep id order (DESIGN R3)
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, deg.p, deg2.p, ids.p, order.p, (int64_t)n, 0, 32, st);
+        }, st, tmp);
+        k_scatter_rank<<<grid_for(n), kThreads, 0, st>>>(order.p, n, h->d_rank.p);
+        PG_LAUNCH_CHECK();
+        PG_CK(cudaStreamSynchronize(st));
+    }
+
+    // ---- S3 orient + relabel ------------------------------------------------
+    keys2.alloc(std::max<uint64_t>(mE, 1));
+    if (mE) {
+        k_orient<<<grid_for(mE), kThreads, 0, st>>>(keys.p, mE, B, h->d_rank.p);
+        PG_LAUNCH_CHECK();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, (int64_t)mE, 0, kbits, st);
+        }, st, tmp);
+    }
+    keys.release();
+    uint64_t* dag = keys2.p;   // DAG edges sorted by (row, col) in rank space
+
+    // ---- S4 cuts ------------------------------------------------------------
+    const uint32_t p = h->p;
+    CutsArg cu{};
+    cu.p = (int)p;
+    {
+        DBuf<uint32_t> dplus, dminus, d_cuts;
+        DBuf<unsigned long long> w, P, d_w;
+        dplus.alloc(n);
+        dminus.alloc(n);
+        w.alloc(n);
+        P.alloc((size_t)n + 1);
+        d_w.alloc(1);
+        d_cuts.alloc(p + 1);
+        PG_CK(cudaMemsetAsync(dplus.p, 0, (size_t)n * 4, st));
+        PG_CK(cudaMemsetAsync(dminus.p, 0, (size_t)n * 4, st));
+        PG_CK(cudaMemsetAsync(d_w.p, 0, 8, st));
+        PG_CK(cudaMemsetAsync(P.p, 0, 8, st));
+        if (mE) {
+            k_dag_degrees<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, dplus.p, dminus.p);
+            PG_LAUNCH_CHECK();
+        }
+        k_cut_weights<<<grid_for(n), kThreads, 0, st>>>(dplus.p, dminus.p, n, (int)h->cut_rule, w.p, d_w.p);
+        PG_LAUNCH_CHECK();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceScan::InclusiveSum(t, b, w.p, P.p + 1, (int64_t)n, st);
+        }, st, tmp);
+        k_cuts<<<1, 128, 0, st>>>(P.p, n, (int)p, d_cuts.p);
+        PG_LAUNCH_CHECK();
+        h->cuts.resize(p + 1);
+        PG_CK(cudaMemcpyAsync(h->cuts.data(), d_cuts.p, (p + 1) * 4, cudaMemcpyDeviceToHost, st));
+        unsigned long long W = 0;
+        PG_CK(cudaMemcpyAsync(&W, d_w.p, 8, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaStreamSynchronize(st));
+        h->wedges = W;
+    }
+    for (uint32_t k = 0; k <= p; ++k) cu.c[k] = h->cuts[k];
+
+    // ---- S5 block CSR -------------------------------------------------------
+    const uint32_t nb = p * p;
+    std::vector<unsigned long long> off(nb + 1, 0);
+    if (mE) {
+        DBuf<uint32_t> bid, bid2;
+        DBuf<uint64_t> dag2;
+        bid.alloc(mE);
+        bid2.alloc(mE);
+        dag2.alloc(mE);
+        k_block_ids<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, bid.p);
+        PG_LAUNCH_CHECK();
+        const int bbits = std::max(1, bits_for(nb - 1));
+        cub_call([&](void* t, size_t& b) {   // stable: (row, col) order kept inside a block
+            return cub::DeviceRadixSort::SortPairs(t, b, bid.p, bid2.p, dag, dag2.p, (int64_t)mE, 0, bbits, st);
+        }, st, tmp);
+        bid.release();
+        DBuf<unsigned long long> d_off;
+        d_off.alloc(nb + 1);
+        k_block_offsets<<<grid_for(nb + 1), kThreads, 0, st>>>(bid2.p, mE, nb, d_off.p);
+        PG_LAUNCH_CHECK();
+        PG_CK(cudaMemcpyAsync(off.data(), d_off.p, (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+        h->d_col.alloc(mE);
+        k_local_cols<<<grid_for(mE), kThreads, 0, st>>>(dag2.p, bid2.p, mE, B, cu, h->d_col.p);
+        PG_LAUNCH_CHECK();
+        PG_CK(cudaStreamSynchronize(st));
+        bid2.release();
+        // dag2 (block-major DAG keys) replaces dag for the rowptr and cost passes
+        PG_CK(cudaMemcpyAsync(dag, dag2.p, mE * 8, cudaMemcpyDeviceToDevice, st));
+        PG_CK(cudaStreamSynchronize(st));
+    }
+    h->blocks.assign(nb, BlockInfo{});
+    uint64_t rp_total = 0;
+    std::vector<BlockDev> bdev(nb);
+    std::vector<unsigned long long> rp_start;
+    std::vector<BlockDev> present;
+    for (uint32_t i = 0; i < p; ++i)
+        for (uint32_t j = 0; j < p; ++j) {
+            BlockInfo& b = h->blocks[i * p + j];
+            b.col_off = off[i * p + j];
+            b.nnz = off[i * p + j + 1] - off[i * p + j];
+            b.nrows = h->cuts[i + 1] - h->cuts[i];
+            b.present = (b.nnz > 0);
+            if (b.present) {
+                b.rp_off = rp_total;
+                rp_start.push_back(rp_total);
+                rp_total += (uint64_t)b.nrows + 1;
+            }
+            bdev[i * p + j] = to_dev(b, h->cuts[i]);
+            if (b.present) present.push_back(bdev[i * p + j]);
+        }
+    h->d_rowptr.alloc(std::max<uint64_t>(rp_total, 1));
+    if (rp_total) {
+        DBuf<BlockDev> d_present;
+        DBuf<unsigned long long> d_rps;
+        d_present.alloc(present.size());
+        d_rps.alloc(rp_start.size());
+        PG_CK(cudaMemcpyAsync(d_present.p, present.data(), present.size() * sizeof(BlockDev),
+                              cudaMemcpyHostToDevice, st));
+        PG_CK(cudaMemcpyAsync(d_rps.p, rp_start.data(), rp_start.size() * 8, cudaMemcpyHostToDevice, st));
+        k_rowptr<<<grid_for(rp_total), kThreads, 0, st>>>(dag, B, d_present.p, d_rps.p, (int)present.size(),
+                                                          rp_total, h->d_rowptr.p);
+        PG_LAUNCH_CHECK();
+        PG_CK(cudaStreamSynchronize(st));
+    }
+
+    // ---- S6 tasks -----------------------------------------------------------
+    h->task_of_ijx.assign((size_t)p * p * p, kNoTask);
+    h->tasks.clear();
+    for (uint32_t i = 0; i < p; ++i)
+        for (uint32_t j = i; j < p; ++j) {
+            if (!h->blocks[i * p + j].present) continue;
+            for (uint32_t x = j; x < p; ++x) {
+                if (!h->blocks[i * p + x].present || !h->blocks[j * p + x].present) continue;
+                h->task_of_ijx[((size_t)i * p + j) * p + x] = (uint32_t)h->tasks.size();
+                Task t;
+                t.i = i; t.j = j; t.x = x;
+                h->tasks.push_back(t);
+            }
+        }
+
+    // ---- S7 costs -----------------------------------------------------------
+    const size_t nt = h->tasks.size();
+    if (nt) {
+        DBuf<uint32_t> d_tid;
+        DBuf<BlockDev> d_blk;
+        DBuf<unsigned long long> d_cost, d_alg;
+        d_tid.alloc(h->task_of_ijx.size());
+        d_blk.alloc(nb);
+        d_cost.alloc(nt);
+        d_alg.alloc(nt);
+        PG_CK(cudaMemcpyAsync(d_tid.p, h->task_of_ijx.data(), h->task_of_ijx.size() * 4, cudaMemcpyHostToDevice, st));
+        PG_CK(cudaMemcpyAsync(d_blk.p, bdev.data(), nb * sizeof(BlockDev), cudaMemcpyHostToDevice, st));
+        PG_CK(cudaMemsetAsync(d_cost.p, 0, nt * 8, st));
+        PG_CK(cudaMemsetAsync(d_alg.p, 0, nt * 8, st));
+        CostArg a;
+        a.dag = dag; a.col = h->d_col.p; a.rowptr = h->d_rowptr.p; a.blk = d_blk.p; a.tid = d_tid.p;
+        a.B = B; a.p = (int)p; a.cu = cu; a.mE = mE; a.cost = d_cost.p; a.alg_el = d_alg.p;
+        k_task_costs<<<grid_for(mE), kThreads, 0, st>>>(a);
+        PG_LAUNCH_CHECK();
+        std::vector<unsigned long long> c(nt), ae(nt);
+        PG_CK(cudaMemcpyAsync(c.data(), d_cost.p, nt * 8, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaMemcpyAsync(ae.data(), d_alg.p, nt * 8, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaStreamSynchronize(st));
+        h->cost_total = 0;
+        h->alg_total = 0;
+        for (size_t t = 0; t < nt; ++t) {
+            Task& T = h->tasks[t];
+            T.cost = c[t];
+            T.alg_el = ae[t];
+            T.alg_bytes = 4 * ae[t] + 12 * h->blocks[T.i * p + T.j].nnz;
+            h->cost_total += T.cost;
+            h->alg_total += T.alg_bytes;
+        }
+    }
+    keys2.release();
+}
+
+// S8: pieces (split heavy tasks by row cost) and LPT over ranks (DESIGN R18).
+void plan_pieces(pgabb_blocks_s* h) {
+    cudaStream_t st = h->stream;
+    const uint32_t p = h->p;
+    const int G = std::max(1, h->world_size);
+    h->pieces.clear();
+    uint64_t total = h->cost_total;
+    const uint64_t cap = (G <= 1) ? ~0ull : std::max<uint64_t>(1, (total + 4ull * G - 1) / (4ull * G));
+    DBuf<unsigned long long> rc, R;
+    DBuf<unsigned char> tmp;
+    for (size_t t = 0; t < h->tasks.size(); ++t) {
+        const Task& T = h->tasks[t];
+        const BlockInfo& bij = h->blocks[T.i * p + T.j];
+        if (T.cost == 0) continue;
+        if (T.cost <= cap) {
+            h->pieces.push_back(Piece{(uint32_t)t, 0, bij.nrows, T.cost, 0});
+            continue;
+        }
+        const uint64_t k = (T.cost + cap - 1) / cap;
+        const uint32_t nr = bij.nrows;
+        rc.alloc((size_t)nr + 1);
+        R.alloc((size_t)nr + 1);
+        PG_CK(cudaMemsetAsync(rc.p, 0, ((size_t)nr + 1) * 8, st));
+        k_row_costs<<<grid_for(nr), kThreads, 0, st>>>(h->d_col.p, h->d_rowptr.p, to_dev(bij, h->cuts[T.i]),
+                                                       to_dev(h->blocks[T.i * p + T.x], 0),
+                                                       to_dev(h->blocks[T.j * p + T.x], 0), rc.p);
+        PG_LAUNCH_CHECK();
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceScan::InclusiveSum(tp, b, rc.p, R.p, (int64_t)nr + 1, st);
+        }, st, tmp);
+        std::vector<unsigned long long> hR((size_t)nr + 1);
+        PG_CK(cudaMemcpyAsync(hR.data(), R.p, ((size_t)nr + 1) * 8, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaStreamSynchronize(st));
+        std::vector<uint32_t> bnd{0};
+        for (uint64_t q = 1; q < k; ++q) {
+            // smallest rho with k * R[rho] >= q * cost
+            const unsigned __int128 tgt = (unsigned __int128)q * T.cost;
+            uint32_t lo = 0, hi = nr;
+            while (lo < hi) {
+                uint32_t mid = lo + ((hi - lo) >> 1);
+                if ((unsigned __int128)k * hR[mid] >= tgt) hi = mid; else lo = mid + 1;
+            }
+            bnd.push_back(lo);
+        }
+        bnd.push_back(nr);
+        for (uint64_t q = 0; q < k; ++q) {
+            const uint64_t c = hR[bnd[q + 1]] - hR[bnd[q]];
+            if (c > 0) h->pieces.push_back(Piece{(uint32_t)t, bnd[q], bnd[q + 1], c, 0});
+        }
+    }
+    // LPT: heaviest first (ties: task, row), least-loaded rank (ties: lowest rank)
+    std::vector<size_t> order(h->pieces.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        const Piece &A = h->pieces[a], &Bp = h->pieces[b];
+        if (A.cost != Bp.cost) return A.cost > Bp.cost;
+        if (A.task != Bp.task) return A.task < Bp.task;
+        return A.r0 < Bp.r0;
+    });
+    using LR = std::pair<uint64_t, int>;
+    std::priority_queue<LR, std::vector<LR>, std::greater<LR>> pq;
+    for (int g = 0; g < G; ++g) pq.push({0, g});
+    for (size_t k : order) {
+        LR top = pq.top();
+        pq.pop();
+        h->pieces[k].owner = top.second;
+        top.first += h->pieces[k].cost;
+        pq.push(top);
+    }
+}
+
+// This rank's work list: owned pieces in (task, row) order with their pool offsets.
+void upload_work(pgabb_blocks_s* h) {
+    const uint32_t p = h->p;
+    const int me = std::max(0, h->rank);
+    h->work.clear();
+    h->work_edges = 0;
+    h->cost_local = 0;
+    h->alg_local = 0;
+    std::vector<char> task_mine(h->tasks.size(), 0);
+    for (const Piece& pc : h->pieces) {
+        if (pc.owner != me) continue;
+        const Task& T = h->tasks[pc.task];
+        const BlockInfo &bij = h->blocks[T.i * p + T.j], &bix = h->blocks[T.i * p + T.x],
+                        &bjx = h->blocks[T.j * p + T.x];
+        uint32_t e0 = 0, e1 = 0;
+        PG_CK(cudaMemcpy(&e0, h->d_rowptr.p + bij.rp_off + pc.r0, 4, cudaMemcpyDeviceToHost));
+        PG_CK(cudaMemcpy(&e1, h->d_rowptr.p + bij.rp_off + pc.r1, 4, cudaMemcpyDeviceToHost));
+        if (e1 == e0) continue;
+        PieceDev w{};
+        w.gstart = h->work_edges;
+        w.col_ij = bij.col_off; w.rp_ij = bij.rp_off;
+        w.col_ix = bix.col_off; w.rp_ix = bix.rp_off;
+        w.col_jx = bjx.col_off; w.rp_jx = bjx.rp_off;
+        w.r0 = pc.r0; w.r1 = pc.r1; w.e0 = e0; w.e1 = e1;
+        w.task = pc.task;
+        h->work.push_back(w);
+        h->work_edges += (e1 - e0);
+        h->cost_local += pc.cost;
+        task_mine[pc.task] = 1;
+    }
+    // staged-model bytes of the owned pieces: whole tasks are attributed to the
+    // rank that owns their first piece's share in proportion to cost
+    for (size_t t = 0; t < h->tasks.size(); ++t) {
+        if (!task_mine[t]) continue;
+        const Task& T = h->tasks[t];
+        uint64_t mine = 0;
+        for (const Piece& pc : h->pieces)
+            if (pc.task == t && pc.owner == me) mine += pc.cost;
+        h->alg_local += (uint64_t)((long double)T.alg_bytes * mine / (T.cost ? T.cost : 1));
+    }
+    h->d_work.alloc(std::max<size_t>(h->work.size(), 1));
+    if (!h->work.empty())
+        PG_CK(cudaMemcpy(h->d_work.p, h->work.data(), h->work.size() * sizeof(PieceDev), cudaMemcpyHostToDevice));
+    h->d_task_counts.alloc(h->tasks.size() + 1);
+    h->d_next.alloc(8);
+}
+
+}  // namespace pgabb

@@ -1,0 +1,173 @@
+// internal.h -- handle layout, error plumbing and small device helpers shared by
+// the build (S1-S8) and count (S9-S11) translation units of libpgabb.so.
+// Nothing here is visible across the C ABI (include/pgabb.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "pgabb.h"
+
+namespace pgabb {
+
+struct Error {
+    pgabb_status_t status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(pgabb_status_t st, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define PG_CK(x) ::pgabb::check_cuda((x), #x, __FILE__, __LINE__)
+#define PG_LAUNCH_CHECK() ::pgabb::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr int kMaxParts = 64;          // p <= 64 (tid table p^3 entries)
+constexpr uint32_t kNoTask = 0xffffffffu;
+
+// Device memory owned by the handle (freed in the destructor / on error unwinding).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) {
+            cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+            if (e != cudaSuccess) {
+                p = nullptr;
+                (void)cudaGetLastError();
+                fail(PGABB_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+            }
+        }
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// Pinned host memory (cudaHostAlloc), for host-resident handles.
+template <class T>
+struct HBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    HBuf() = default;
+    HBuf(const HBuf&) = delete;
+    HBuf& operator=(const HBuf&) = delete;
+    ~HBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) {
+            cudaError_t e = cudaHostAlloc(&p, count * sizeof(T), cudaHostAllocDefault);
+            if (e != cudaSuccess) {
+                p = nullptr;
+                (void)cudaGetLastError();
+                fail(PGABB_ENOMEM, "cudaHostAlloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+            }
+        }
+        n = count;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// One block A_ij of the p x p grid (only i <= j can be non-empty: the DAG is
+// upper triangular in rank space, DESIGN R4).  Pools are block-major.
+struct BlockInfo {
+    uint64_t nnz = 0;
+    uint64_t col_off = 0;   // first edge in the col pool
+    uint64_t rp_off = 0;    // first rowptr entry in the rowptr pool (nrows+1 entries)
+    uint32_t nrows = 0;     // cut_{i+1} - cut_i
+    uint32_t present = 0;   // nnz > 0 (rowptr stored)
+};
+
+struct Task {
+    uint32_t i, j, x;
+    uint64_t cost = 0;       // S7: sum_{(u,v) in A_ij} (|A_ix[u]| + |A_jx[v]|)
+    uint64_t alg_el = 0;     // staged-model elements (DESIGN R19)
+    uint64_t alg_bytes = 0;  // 4*alg_el + 12*nnz(A_ij)
+};
+
+struct Piece {
+    uint32_t task;
+    uint32_t r0, r1;         // local rows of part i
+    uint64_t cost;
+    int32_t owner;
+};
+
+// Work-list entry for the intersection kernels (one per owned piece).
+struct PieceDev {
+    uint64_t gstart;         // first position in this rank's flattened edge space
+    uint64_t col_ij, rp_ij;  // pool offsets of A_ij
+    uint64_t col_ix, rp_ix;  // pool offsets of A_ix
+    uint64_t col_jx, rp_jx;  // pool offsets of A_jx
+    uint32_t r0, r1;         // local row range of the piece
+    uint32_t e0, e1;         // edge range (block-local) = rowptr_ij[r0], rowptr_ij[r1]
+    uint32_t task;
+    uint32_t pad;
+};
+
+}  // namespace pgabb
+
+struct pgabb_blocks_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t n = 0;
+    uint64_t m_tuples = 0, m_edges = 0;
+    uint32_t p = 1;
+    uint32_t cut_rule = 0;
+    int32_t rank = 0, world_size = 1;
+    uint32_t residency = PGABB_RESIDENT_DEVICE;
+    uint64_t budget = 0;
+    uint64_t wedges = 0;
+
+    std::vector<uint32_t> cuts;                 // p+1
+    std::vector<pgabb::BlockInfo> blocks;       // p*p, row-major block id i*p+j
+    std::vector<pgabb::Task> tasks;             // (i,j,x) lexicographic
+    std::vector<pgabb::Piece> pieces;           // (task, row) order
+    std::vector<uint32_t> task_of_ijx;          // p^3 -> task id or kNoTask
+
+    pgabb::DBuf<uint32_t> d_rank;               // original id -> rank
+    pgabb::DBuf<uint32_t> d_col;                // col pool (local col ids), block-major
+    pgabb::DBuf<uint32_t> d_rowptr;             // rowptr pool (block-local edge offsets)
+    pgabb::HBuf<uint32_t> h_col, h_rowptr;      // host-resident copies (RESIDENT_HOST)
+
+    // this rank's work list
+    std::vector<pgabb::PieceDev> work;
+    uint64_t work_edges = 0;
+    pgabb::DBuf<pgabb::PieceDev> d_work;
+    pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
+    pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
+    pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+
+    // stats
+    uint64_t cost_total = 0, cost_local = 0, alg_total = 0, alg_local = 0;
+    uint64_t h2d_last = 0, launches_last = 0;
+    double ms_build = 0, ms_count_last = 0, ms_main_last = 0;
+    bool timing_pending = false;   // events of the last (async) count not read yet
+
+    ~pgabb_blocks_s();
+};
+
+namespace pgabb {
+void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint32_t* dst, bool on_device);
+void plan_pieces(pgabb_blocks_s* h);
+void upload_work(pgabb_blocks_s* h);
+uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote);
+void resolve_timing(pgabb_blocks_s* h);
+}  // namespace pgabb

@@ -1,0 +1,44 @@
+"""Multi-GPU driver: one process per GPU (torchrun), tasks split by LPT (S8) and
+the per-rank uint64 counts combined with ONE NCCL allreduce of 8 bytes (S11).
+
+torch.distributed is plumbing here: it provides the process group and the
+NCCL allreduce of the per-rank count, which the library writes straight into
+a device int64 tensor on the same stream (no host round trip before the
+collective).  Counts are < 2^63, so int64 is exact.
+"""
+from __future__ import annotations
+
+from . import Blocks, build_blocks
+
+
+def build_blocks_for_rank(n, src, dst, p=0, cut_rule=0, residency=0, device_budget_bytes=0, group=None):
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    ws = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,
+                        residency=residency, device_budget_bytes=device_budget_bytes)
+
+
+def triangle_count_allreduce(b: Blocks, out=None, group=None) -> int:
+    """This rank's count -> device int64 -> NCCL allreduce(sum) -> host int."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    if out is None:
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    b.triangle_count(stream=stream.cuda_stream, d_count=out.data_ptr(), sync=False)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return int(out.item())
+
+
+def combine_counts_host(local: int, group=None) -> int:
+    """Allreduce of host-side partial counts (CPU/gloo path used by the tests)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([local], dtype=torch.int64)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())

@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact.
+
+All arithmetic is integer, so the bar is exact equality for every step:
+rank (S2), cuts (S4), block CSR (S5), tasks (S6), costs and algorithmic bytes
+(S7), pieces and LPT owners (S8), per-task counts (S10) and the total (S11).
+"""
+from math import comb
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import oracle.blocks as ob
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2209_04541_b200 as pg  # noqa: E402
+
+
+def gpu_T(g, **kw):
+    with pg.build_blocks(*g, **kw) as b:
+        return b.triangle_count()
+
+
+# ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+def test_closed_forms(p):
+    cases = [
+        (gen.complete(3), 1), (gen.complete(4), 4), (gen.complete(57), comb(57, 3)),
+        (gen.cycle(3), 1), (gen.cycle(100), 0), (gen.path(50), 0), (gen.star(40), 0),
+        (gen.wheel(4), 4), (gen.wheel(5), 4), (gen.wheel(300), 299),
+        (gen.windmill(7, 6), 7 * comb(6, 3)), (gen.rook(5, 7), 7 * comb(5, 3) + 5 * comb(7, 3)),
+        (gen.king(17, 23), 4 * 16 * 22), (gen.complete_bipartite(9, 13), 0),
+        (gen.clique_union([3, 9, 200, 2, 1, 64]), sum(comb(s, 3) for s in [3, 9, 200, 2, 1, 64])),
+        (gen.random_tree(500, 3), 0),
+    ]
+    for g, want in cases:
+        assert gpu_T(g, p=p) == want, (g[0], want)
+
+
+def test_grid_diagonals_closed_form():
+    for side, f in [(64, 0.0), (200, 0.1), (513, 0.5), (33, 1.0)]:
+        g = gen.grid(side, f, seed=2)
+        assert gpu_T(g, p=5) == 2 * gen.grid_ndiag(side, f, seed=2)
+
+
+def test_degenerate_inputs():
+    e = np.zeros(0, np.uint32)
+    assert gpu_T((0, e, e), p=4) == 0
+    assert gpu_T((10, e, e), p=4) == 0
+    loops = np.arange(5, dtype=np.uint32)
+    assert gpu_T((5, loops, loops), p=2) == 0                    # only self-loops
+    assert gpu_T((2, np.array([0, 1, 0], np.uint32), np.array([1, 0, 1], np.uint32)), p=2) == 0
+    assert gpu_T((1, np.array([0], np.uint32), np.array([0], np.uint32)), p=3) == 0
+
+
+def test_errors():
+    with pytest.raises(pg.PgabbError) as e:
+        pg.build_blocks(3, np.array([0, 3], np.uint32), np.array([1, 1], np.uint32))
+    assert e.value.name == "EINVAL"
+    with pytest.raises(pg.PgabbError) as e:
+        pg.build_blocks(3, np.array([0], np.uint32), np.array([1], np.uint32), rank=2, world_size=2)
+    assert e.value.name == "EINVAL"
+    with pytest.raises(pg.PgabbError):
+        pg.build_blocks(3, np.array([0], np.uint32), np.array([1], np.uint32), cut_rule=7)
+
+
+# ---------------------------------------------------------------- totals vs oracle
+@pytest.mark.parametrize("scale", [6, 10, 13, 16])
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 16])
+def test_rmat_total_vs_oracle(scale, p):
+    g = gen.rmat(scale, 16, seed=scale)
+    assert gpu_T(g, p=p) == oracle.count(*g)
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_er_grid_total_vs_oracle(rule):
+    for g in (gen.er(1 << 15, 32, seed=3), gen.er(1000, 8, seed=4), gen.grid(300, 0.2, seed=5)):
+        assert gpu_T(g, p=7, cut_rule=rule) == oracle.count(*g)
+
+
+def test_messy_and_relabel_invariance():
+    g = gen.rmat(12, 16, seed=9)
+    want = oracle.count(*g)
+    assert gpu_T(gen.messy(g, seed=1), p=4) == want
+    assert gpu_T(gen.relabel(g, seed=2), p=4) == want
+
+
+def test_device_inputs():
+    g = gen.rmat(12, 16, seed=10)
+    s = torch.from_numpy(g[1].view(np.int32)).cuda()
+    d = torch.from_numpy(g[2].view(np.int32)).cuda()
+    with pg.build_blocks(g[0], s, d, p=6) as b:
+        assert b.triangle_count() == oracle.count(*g)
+
+
+def test_repeat_deterministic():
+    g = gen.rmat(14, 16, seed=11)
+    with pg.build_blocks(*g, p=8) as b:
+        r = [b.triangle_count(task_counts=True) for _ in range(3)]
+    assert all(x[0] == r[0][0] for x in r)
+    assert all((x[1] == r[0][1]).all() for x in r)
+
+
+def test_host_residency():
+    g = gen.rmat(13, 16, seed=12)
+    with pg.build_blocks(*g, p=4, residency=pg.RESIDENT_HOST) as b:
+        assert b.triangle_count() == oracle.count(*g)
+        assert b.stats()["h2d_bytes_last"] > 0
+
+
+# ---------------------------------------------------------------- step-by-step parity
+SMALL = [
+    ("rmat9", lambda: gen.rmat(9, 16, seed=1)),
+    ("er", lambda: gen.er_small(300, 0.05, seed=2)),
+    ("king", lambda: gen.king(9, 11)),
+    ("messy", lambda: gen.messy(gen.rmat(8, 8, seed=3), seed=3)),
+]
+
+
+@pytest.mark.parametrize("name,mk", SMALL)
+@pytest.mark.parametrize("p,rule", [(1, 0), (2, 0), (3, 1), (5, 0), (8, 1)])
+def test_steps_parity(name, mk, p, rule):
+    g = mk()
+    P = ob.Plan(*g, p=p, rule=rule)
+    with pg.build_blocks(*g, p=p, cut_rule=rule) as b:
+        st = b.stats()
+        assert st["m_edges"] == len(P.E)
+        assert st["p"] == P.p
+        assert (b.rank() == P.rank).all()                                    # S2
+        assert list(b.cuts()) == list(P.cuts)                                # S4
+        for (i, j), (rp, col) in P.B.items():                                # S5
+            grp, gcol = b.block(i, j)
+            assert list(gcol) == list(col), (i, j)
+            if col.size:
+                assert list(grp) == list(rp), (i, j)
+        ijx, cost, alg = b.tasks()                                           # S6, S7
+        assert [tuple(map(int, t)) for t in ijx] == P.tasks
+        assert list(map(int, cost)) == P.costs
+        assert list(map(int, alg)) == P.alg_bytes
+        assert st["wedges"] == ob.wedges_dag(g[0], P.D)
+        T, tc = b.triangle_count(task_counts=True)                           # S10, S11
+        assert list(map(int, tc)) == P.task_counts()
+        assert T == oracle.count(*g)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_pieces_lpt_and_rank_sum(G):
+    g = gen.rmat(10, 16, seed=21)
+    P = ob.Plan(*g, p=4, G=G)
+    total = 0
+    for r in range(G):   # logical-rank simulation on one GPU
+        with pg.build_blocks(*g, p=4, rank=r, world_size=G) as b:
+            pcs, owner = b.pieces()
+            assert pcs == P.pieces                                           # S8 pieces
+            assert owner == P.owner                                          # S8 LPT
+            T_r, tc = b.triangle_count(task_counts=True)
+            want = sum(ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2])
+                       for pc, o in zip(P.pieces, P.owner) if o == r)
+            assert T_r == want
+            total += T_r
+    assert total == oracle.count(*g)
