@@ -207,7 +207,10 @@ def run_ours(args):
     b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy-default) stream: the library orders its work on it and the
+    # CUDA events below are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 

@@ -65,6 +65,10 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_next.release();
     h_col.release();
     h_rowptr.release();
+    h_bitmap.release();
+    d_bitmap.release();
+    d_tasks.release();
+    d_items.release();
     h_result.release();
     for (cudaEvent_t e : {ev0, ev1, ev2, ev3})
         if (e) cudaEventDestroy(e);
@@ -135,6 +139,9 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
             if (h->d_col.n) PG_CK(cudaMemcpy(h->h_col.p, h->d_col.p, h->d_col.bytes(), cudaMemcpyDeviceToHost));
             if (h->d_rowptr.n)
                 PG_CK(cudaMemcpy(h->h_rowptr.p, h->d_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyDeviceToHost));
+            h->h_bitmap.alloc(h->d_bitmap.n);
+            if (h->d_bitmap.n)
+                PG_CK(cudaMemcpy(h->h_bitmap.p, h->d_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyDeviceToHost));
         }
         PG_CK(cudaStreamSynchronize(h->stream));
         h->ms_build = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -176,7 +183,7 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->cost_local = b->cost_local;
         s->alg_bytes_total = b->alg_total;
         s->alg_bytes_local = b->alg_local;
-        s->block_bytes = b->d_col.bytes() + b->d_rowptr.bytes();
+        s->block_bytes = b->d_col.bytes() + b->d_rowptr.bytes() + b->d_bitmap.bytes();
         s->h2d_bytes_last = b->h2d_last;
         s->launches_last = b->launches_last;
         s->ms_build = b->ms_build;

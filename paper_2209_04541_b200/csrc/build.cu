@@ -262,6 +262,46 @@ __global__ void k_row_costs(const uint32_t* col, const uint32_t* rowptr, BlockDe
     }
 }
 
+// Dense copy of one block: row r's bits over the column part, one thread per row
+// (each row's words are owned by one thread, so no atomics).
+__global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsigned long long col_off,
+                              unsigned long long rp_off, uint32_t nrows, uint32_t words, uint32_t* bm) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nrows;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t* row = bm + r * words;
+        for (uint32_t k = 0; k < words; ++k) row[k] = 0u;
+        const uint32_t e0 = rowptr[rp_off + r], e1 = rowptr[rp_off + r + 1];
+        for (uint32_t e = e0; e < e1; ++e) {
+            const uint32_t c = col[col_off + e];
+            row[c >> 5] |= 1u << (c & 31);
+        }
+    }
+}
+
+// Row items of one owned piece: rows u in [r0, r1) with A_ij[u] and A_ix[u]
+// non-empty, with their estimated work |A_ix[u]| + sum_v |A_jx[v]| (the staged
+// model's element count for the row).  out == nullptr: count only.
+__global__ void k_row_items(PieceDev w, const uint32_t* col, const uint32_t* rowptr, unsigned long long* out,
+                            uint32_t* out_work, unsigned long long* counter) {
+    for (uint64_t r = w.r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < w.r1;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)r;
+        const uint32_t e0 = rowptr[w.rp_ij + u], e1 = rowptr[w.rp_ij + u + 1];
+        if (e0 == e1) continue;
+        const uint32_t la = rowptr[w.rp_ix + u + 1] - rowptr[w.rp_ix + u];
+        if (la == 0) continue;
+        const unsigned long long idx = atomicAdd(counter, 1ull);
+        if (!out) continue;
+        unsigned long long work = la;
+        for (uint32_t e = e0; e < e1; ++e) {
+            const uint32_t v = col[w.col_ij + e];
+            work += rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v];
+        }
+        out[idx] = ((unsigned long long)w.task << 32) | u;
+        out_work[idx] = (uint32_t)min(work, 0xffffffffull);
+    }
+}
+
 template <class F>
 void cub_call(F f, cudaStream_t st, DBuf<unsigned char>& tmp) {
     size_t bytes = 0;
@@ -493,6 +533,31 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_CK(cudaStreamSynchronize(st));
     }
 
+    // ---- S5b dense bitmap copies of dense, narrow blocks -----
+    {
+        uint64_t words_total = 0;
+        for (uint32_t i = 0; i < p; ++i)
+            for (uint32_t j = i; j < p; ++j) {
+                BlockInfo& b = h->blocks[i * p + j];
+                const uint64_t wj = h->cuts[j + 1] - h->cuts[j];
+                if (!b.present || wj > kWarpBitmapBits) continue;
+                if (b.nnz * kDenseInv < (uint64_t)b.nrows * wj) continue;   // density < 1/32
+                b.bm_words = (uint32_t)((wj + 31) / 32);
+                b.bm_off = words_total;
+                words_total += (uint64_t)b.nrows * b.bm_words;
+            }
+        h->d_bitmap.alloc(std::max<uint64_t>(words_total, 1));
+        for (uint32_t i = 0; i < p; ++i)
+            for (uint32_t j = i; j < p; ++j) {
+                const BlockInfo& b = h->blocks[i * p + j];
+                if (b.bm_off == ~0ull) continue;
+                k_fill_bitmap<<<grid_for(b.nrows), kThreads, 0, st>>>(h->d_col.p, h->d_rowptr.p, b.col_off, b.rp_off,
+                                                                      b.nrows, b.bm_words, h->d_bitmap.p + b.bm_off);
+                PG_LAUNCH_CHECK();
+            }
+        PG_CK(cudaStreamSynchronize(st));
+    }
+
     // ---- S6 tasks -----------------------------------------------------------
     h->task_of_ijx.assign((size_t)p * p * p, kNoTask);
     h->tasks.clear();
@@ -661,6 +726,60 @@ void upload_work(pgabb_blocks_s* h) {
         PG_CK(cudaMemcpy(h->d_work.p, h->work.data(), h->work.size() * sizeof(PieceDev), cudaMemcpyHostToDevice));
     h->d_task_counts.alloc(h->tasks.size() + 1);
     h->d_next.alloc(8);
+
+    // task descriptors for the intersection kernel
+    std::vector<TaskDev> td(std::max<size_t>(h->tasks.size(), 1));
+    for (size_t t = 0; t < h->tasks.size(); ++t) {
+        const Task& T = h->tasks[t];
+        const BlockInfo &bij = h->blocks[T.i * p + T.j], &bix = h->blocks[T.i * p + T.x],
+                        &bjx = h->blocks[T.j * p + T.x];
+        TaskDev d{};
+        d.col_ij = bij.col_off; d.rp_ij = bij.rp_off;
+        d.col_ix = bix.col_off; d.rp_ix = bix.rp_off;
+        d.col_jx = bjx.col_off; d.rp_jx = bjx.rp_off;
+        d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
+        d.bm_jx = bjx.bm_off;
+        d.bm_words = bjx.bm_words;
+        td[t] = d;
+    }
+    h->d_tasks.alloc(td.size());
+    PG_CK(cudaMemcpy(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
+
+    // row items of the owned pieces, heaviest first (in-GPU analogue of the paper's
+    // "sorts them in decreasing order")
+    cudaStream_t st = h->stream;
+    DBuf<unsigned long long> cnt;
+    cnt.alloc(1);
+    PG_CK(cudaMemsetAsync(cnt.p, 0, 8, st));
+    for (const PieceDev& w : h->work) {
+        k_row_items<<<grid_for(w.r1 - w.r0), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, nullptr, nullptr,
+                                                                 cnt.p);
+        PG_LAUNCH_CHECK();
+    }
+    unsigned long long nitems = 0;
+    PG_CK(cudaMemcpyAsync(&nitems, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    PG_CK(cudaStreamSynchronize(st));
+    h->n_items = nitems;
+    h->d_items.alloc(std::max<uint64_t>(nitems, 1));
+    if (nitems) {
+        DBuf<unsigned long long> items;
+        DBuf<uint32_t> wk, wk2;
+        DBuf<unsigned char> tmp;
+        items.alloc(nitems);
+        wk.alloc(nitems);
+        wk2.alloc(nitems);
+        PG_CK(cudaMemsetAsync(cnt.p, 0, 8, st));
+        for (const PieceDev& w : h->work) {
+            k_row_items<<<grid_for(w.r1 - w.r0), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, items.p, wk.p,
+                                                                     cnt.p);
+            PG_LAUNCH_CHECK();
+        }
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceRadixSort::SortPairsDescending(tp, b, wk.p, wk2.p, items.p, h->d_items.p,
+                                                             (int64_t)nitems, 0, 32, st);
+        }, st, tmp);
+        PG_CK(cudaStreamSynchronize(st));
+    }
 }
 
 }  // namespace pgabb

@@ -15,9 +15,6 @@ namespace pgabb {
 
 namespace {
 
-constexpr int kWarpsPerCta = 8;
-constexpr int kChunk = 32;   // edges a warp claims per atomic grab
-
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;
@@ -43,55 +40,173 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
     return c;
 }
 
-// One warp per edge (u,v) of A_ij; warps claim chunks of kChunk consecutive
-// edges of the rank's flattened edge space dynamically.  Per-task partial counts
-// are flushed with one atomicAdd per (chunk, task) run.
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
-k_tc_warp(const PieceDev* __restrict__ work, int nwork, unsigned long long total_edges,
-          const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
-          unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ next) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(next, (unsigned long long)kChunk);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= total_edges) break;
-        const unsigned long long end = min(base + kChunk, total_edges);
-        // piece containing `base`: last piece with gstart <= base
-        int lo = 0, hi = nwork;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (work[mid].gstart <= base) lo = mid; else hi = mid;
+// ---------------------------------------------------------------------------
+// k_tc_rows: one warp per row item (task t = (i,j,x), row u of part i).
+//
+//   stage    A_ix[u] into a warp-private shared-memory set over part x:
+//            a bitmap of w_x bits (w_x <= 32768, 4 KB) or, for wider parts, an
+//            open-addressing hash of <= 1024 slots (|A_ix[u]| <= 512);
+//   stream   the lists A_jx[v] of 32 consecutive v in A_ij[u] at a time, as
+//            one flattened sequence: lane l takes positions l, l+32, ... and
+//            finds its v by a 5-step shuffle search over the warp's prefix of
+//            list lengths, so short lists do not idle lanes (load-balanced
+//            "merge-path" over the batch); reads are coalesced within a list;
+//   probe    each element against the staged set;
+//   reduce   lane partials -> warp sum -> one atomicAdd into the task's count.
+//
+// Rows whose A_ix[u] fits neither set fall back to lane-parallel binary search.
+// This is the staged model of SURVEY §8(d): A_ix[u] read once per (task, u),
+// A_jx[v] once per edge.  Items arrive sorted by estimated work (heaviest
+// first) and are dealt cyclically to the warps of the grid (no atomics).
+// ---------------------------------------------------------------------------
+constexpr int kRowWarps = 8;
+constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
+    return (w * 2654435761u) >> (32 - hbits);
+}
+
+template <int MODE>
+__device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask) {
+    if (MODE == 0) return (S[w >> 5] >> (w & 31)) & 1u;
+    uint32_t h = hash_slot(w, hbits), s;
+    while ((s = S[h]) != 0u && s != w + 1) h = (h + 1) & hmask;
+    return s == w + 1;
+}
+
+// Stream the lists of A_jx[v] for v in A_ij[u] (edges e0..e1) against the set S.
+template <int MODE>
+__device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
+                                               const uint32_t* __restrict__ rp_jx,
+                                               const uint32_t* __restrict__ Bc, const uint32_t* S,
+                                               uint32_t hbits, uint32_t hmask, int lane) {
+    uint32_t acc = 0;
+    for (uint32_t e = e0; e < e1; e += 32) {
+        uint32_t b0 = 0, lb = 0;
+        if (e + lane < e1) {
+            const uint32_t v = __ldg(vcol + e + lane);
+            b0 = __ldg(rp_jx + v);
+            lb = __ldg(rp_jx + v + 1) - b0;
         }
-        int pc = lo;
-        PieceDev w = work[pc];
-        uint32_t e = w.e0 + (uint32_t)(base - w.gstart);   // block-local edge index
-        // row containing edge e: last u in [r0, r1) with rowptr[u] <= e
-        uint32_t a = w.r0, z = w.r1;
-        while (z - a > 1) {
-            const uint32_t mid = (a + z) >> 1;
-            if (__ldg(rowptr + w.rp_ij + mid) <= e) a = mid; else z = mid;
+        uint32_t incl = lb;   // inclusive prefix of list lengths over the batch
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        uint32_t u = a;
-        uint32_t acc = 0;
-        for (unsigned long long g = base; g < end; ++g, ++e) {
-            if (e >= w.e1) {   // next piece
-                const unsigned long long s = warp_sum(acc);
-                if (lane == 0 && s) atomicAdd(&task_counts[w.task], s);
-                acc = 0;
-                w = work[++pc];
-                e = w.e0;
-                u = w.r0;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - lb;
+        for (uint32_t base = 0; base < total; base += 64) {
+            uint32_t w[2];
+            bool ok[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t pos = base + r * 32 + lane;
+                // largest segment q with excl_q <= pos
+                uint32_t lo = 0;
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + stp);
+                    if (ex <= pos) lo += stp;
+                }
+                const uint32_t sb = __shfl_sync(0xffffffffu, b0, lo);
+                const uint32_t se = __shfl_sync(0xffffffffu, excl, lo);
+                ok[r] = pos < total;
+                w[r] = ok[r] ? __ldg(Bc + sb + (pos - se)) : 0u;
             }
-            while (__ldg(rowptr + w.rp_ij + u + 1) <= e) ++u;
-            const uint32_t v = __ldg(col + w.col_ij + e);
-            const uint32_t a0 = __ldg(rowptr + w.rp_ix + u), a1 = __ldg(rowptr + w.rp_ix + u + 1);
-            const uint32_t b0 = __ldg(rowptr + w.rp_jx + v), b1 = __ldg(rowptr + w.rp_jx + v + 1);
-            if (a1 > a0 && b1 > b0)
-                acc += warp_intersect(col + w.col_ix + a0, a1 - a0, col + w.col_jx + b0, b1 - b0, lane);
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (ok[r]) acc += probe<MODE>(S, w[r], hbits, hmask);
         }
-        const unsigned long long s = warp_sum(acc);
-        if (lane == 0 && s) atomicAdd(&task_counts[w.task], s);
+    }
+    return acc;
+}
+
+// Dense A_jx (bitmap rows of W words): |A_ix[u] ∩ A_jx[v]| = sum_k popc(S[k] & row_v[k]).
+// The warp is split into G = 32/gsz groups (gsz = pow2 >= W, capped at 32), one
+// v per group, so narrow parts keep every lane busy.
+__device__ __forceinline__ uint32_t and_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
+                                            const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
+                                            int lane) {
+    uint32_t gsz = 1;
+    while (gsz < W && gsz < 32) gsz <<= 1;
+    const uint32_t G = 32 / gsz, g = lane / gsz, kl = lane % gsz;
+    uint32_t acc = 0;
+    for (uint32_t e = e0; e < e1; e += 32) {
+        const uint32_t nb = min(32u, e1 - e);
+        const uint32_t v = ((uint32_t)lane < nb) ? __ldg(vcol + e + lane) : 0u;
+        for (uint32_t q = 0; q < nb; q += G) {
+            const uint32_t qq = q + g;
+            const uint32_t vq = __shfl_sync(0xffffffffu, v, qq & 31);
+            if (qq < nb) {
+                const uint32_t* __restrict__ row = BM + (uint64_t)vq * W;
+                for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + k));
+            }
+        }
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32)
+k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitems,
+          const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
+          const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
+          unsigned long long* __restrict__ task_counts) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* S = smem + wid * kSetWords;
+    for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
+    __syncwarp();
+    const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
+    for (unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid; idx < nitems; idx += nwarps) {
+        const unsigned long long it = items[idx];
+        const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
+        const TaskDev T = tasks[t];
+        const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
+        const uint32_t e0 = __ldg(rowptr + T.rp_ij + u), e1 = __ldg(rowptr + T.rp_ij + u + 1);
+        const uint32_t la = a1 - a0;
+        const uint32_t* __restrict__ A = col + T.col_ix + a0;
+        const uint32_t* __restrict__ Bc = col + T.col_jx;
+        const uint32_t* __restrict__ vcol = col + T.col_ij;
+        const uint32_t* __restrict__ rp_jx = rowptr + T.rp_jx;
+        const int mode = (T.wx <= kWarpBitmapBits) ? 0 : (la <= kHashMaxList ? 1 : 2);
+        uint32_t hbits = 5;
+        while ((1u << hbits) < 2 * la) ++hbits;
+        const uint32_t hmask = (1u << hbits) - 1;
+        uint32_t acc = 0;
+        if (mode == 0) {
+            for (uint32_t k = lane; k < la; k += 32) {
+                const uint32_t w = __ldg(A + k);
+                atomicOr(&S[w >> 5], 1u << (w & 31));
+            }
+            __syncwarp();
+            if (T.bm_jx != ~0ull)
+                acc = and_row(vcol, e0, e1, bitmap + T.bm_jx, T.bm_words, S, lane);
+            else
+                acc = stream_row<0>(vcol, e0, e1, rp_jx, Bc, S, hbits, hmask, lane);
+            __syncwarp();
+            for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
+        } else if (mode == 1) {
+            for (uint32_t k = lane; k < la; k += 32) {
+                const uint32_t w = __ldg(A + k);
+                uint32_t h = hash_slot(w, hbits);
+                while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
+            }
+            __syncwarp();
+            acc = stream_row<1>(vcol, e0, e1, rp_jx, Bc, S, hbits, hmask, lane);
+            __syncwarp();
+            for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
+        } else {
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t v = __ldg(vcol + e);
+                const uint32_t b0 = __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
+                if (b1 > b0) acc += warp_intersect(A, la, Bc + b0, b1 - b0, lane);
+            }
+        }
+        __syncwarp();
+        const unsigned long long sum = warp_sum(acc);
+        if (lane == 0 && sum) atomicAdd(&task_counts[t], sum);
     }
 }
 
@@ -138,17 +253,26 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     if (h->residency == PGABB_RESIDENT_HOST && h->d_col.n) {
         PG_CK(cudaMemcpyAsync(h->d_col.p, h->h_col.p, h->d_col.bytes(), cudaMemcpyHostToDevice, st));
         PG_CK(cudaMemcpyAsync(h->d_rowptr.p, h->h_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyHostToDevice, st));
-        h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes();
+        PG_CK(cudaMemcpyAsync(h->d_bitmap.p, h->h_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyHostToDevice, st));
+        h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes() + h->d_bitmap.bytes();
     }
     PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
-    PG_CK(cudaMemsetAsync(h->d_next.p, 0, 8 * sizeof(unsigned long long), st));
     PG_CK(cudaEventRecord(h->ev1, st));
-    if (h->work_edges) {
-        int dev_sms = 148;
-        PG_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
-        const unsigned grid = (unsigned)dev_sms * 8;
-        k_tc_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(h->d_work.p, (int)h->work.size(), h->work_edges,
-                                                     h->d_col.p, h->d_rowptr.p, h->d_task_counts.p, h->d_next.p);
+    if (h->n_items) {
+        static thread_local int cached_dev = -1, grid = 0;
+        const size_t smem = kRowWarps * kSetWords * sizeof(uint32_t);
+        if (cached_dev != h->device) {
+            PG_CK(cudaFuncSetAttribute(k_tc_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int sms = 0, per_sm = 0;
+            PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+            PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows, kRowWarps * 32, smem));
+            grid = sms * std::max(per_sm, 1);
+            cached_dev = h->device;
+        }
+        unsigned g = (unsigned)std::min<unsigned long long>((unsigned long long)grid,
+                                                            (h->n_items + kRowWarps - 1) / kRowWarps);
+        k_tc_rows<<<g, kRowWarps * 32, smem, st>>>(h->d_items.p, h->n_items, h->d_tasks.p, h->d_col.p,
+                                                   h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p);
         PG_LAUNCH_CHECK();
         h->launches_last++;
     }

@@ -92,6 +92,8 @@ struct BlockInfo {
     uint64_t rp_off = 0;    // first rowptr entry in the rowptr pool (nrows+1 entries)
     uint32_t nrows = 0;     // cut_{i+1} - cut_i
     uint32_t present = 0;   // nnz > 0 (rowptr stored)
+    uint64_t bm_off = ~0ull; // dense copy: first word in the bitmap pool (~0: none)
+    uint32_t bm_words = 0;   // words per bitmap row = ceil(width of column part / 32)
 };
 
 struct Task {
@@ -120,6 +122,26 @@ struct PieceDev {
     uint32_t pad;
 };
 
+// Per-task descriptor read by the intersection kernel.
+struct TaskDev {
+    uint64_t col_ij, rp_ij;  // pool offsets of A_ij
+    uint64_t col_ix, rp_ix;  // pool offsets of A_ix
+    uint64_t col_jx, rp_jx;  // pool offsets of A_jx
+    uint64_t bm_jx;          // bitmap-pool offset of dense A_jx rows, ~0 if A_jx is list-only
+    uint32_t wx;             // width of column part x (bits of a bitmap over it)
+    uint32_t bm_words;       // words per dense row of A_jx
+};
+
+// A block gets a dense bitmap copy (rows of ceil(w/32) words) when its density is
+// at least 1/kDenseInv and its column part is narrow enough for a warp bitmap:
+// then the copy is no larger than the list form.
+constexpr uint64_t kDenseInv = 32;
+
+// A row item: (task, local row u of part i) with A_ij[u] and A_ix[u] non-empty.
+// Packed as (task << 32) | u; items are sorted by estimated work, heaviest first.
+constexpr uint32_t kWarpBitmapBits = 32768;   // per-warp smem bitmap: 4 KB
+constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
+
 }  // namespace pgabb
 
 struct pgabb_blocks_s {
@@ -143,12 +165,16 @@ struct pgabb_blocks_s {
     pgabb::DBuf<uint32_t> d_rank;               // original id -> rank
     pgabb::DBuf<uint32_t> d_col;                // col pool (local col ids), block-major
     pgabb::DBuf<uint32_t> d_rowptr;             // rowptr pool (block-local edge offsets)
-    pgabb::HBuf<uint32_t> h_col, h_rowptr;      // host-resident copies (RESIDENT_HOST)
+    pgabb::DBuf<uint32_t> d_bitmap;             // dense-block bitmap pool (rows of bm_words)
+    pgabb::HBuf<uint32_t> h_col, h_rowptr, h_bitmap;   // host-resident copies (RESIDENT_HOST)
 
     // this rank's work list
     std::vector<pgabb::PieceDev> work;
     uint64_t work_edges = 0;
     pgabb::DBuf<pgabb::PieceDev> d_work;
+    pgabb::DBuf<pgabb::TaskDev> d_tasks;             // ntasks descriptors
+    pgabb::DBuf<unsigned long long> d_items;         // row items, heaviest first
+    uint64_t n_items = 0;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
     pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
