@@ -75,11 +75,19 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
 }
 
 // Stream the lists of A_jx[v] for v in A_ij[u] (edges e0..e1) against the set S.
+// The non-empty lists of a batch of 32 v are compacted (ballot + popc) and their
+// "index delta" (list start - flattened start) parked in 32 words of warp
+// scratch; in each round of 32 flattened positions, the segment of position
+// base+l is cur + popc(starts in (base, base+l]), where the start mask comes from
+// one __reduce_or_sync and cur from one ballot -- no per-position search.
 template <int MODE>
 __device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                const uint32_t* __restrict__ rp_jx,
                                                const uint32_t* __restrict__ Bc, const uint32_t* S,
-                                               uint32_t hbits, uint32_t hmask, int lane) {
+                                               uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
+                                               int lane) {
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t le_mask = 0xffffffffu >> (31 - lane);
     uint32_t acc = 0;
     for (uint32_t e = e0; e < e1; e += 32) {
         uint32_t b0 = 0, lb = 0;
@@ -88,6 +96,8 @@ __device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol
             b0 = __ldg(rp_jx + v);
             lb = __ldg(rp_jx + v + 1) - b0;
         }
+        const uint32_t nonempty = __ballot_sync(0xffffffffu, lb > 0);
+        if (nonempty == 0u) continue;
         uint32_t incl = lb;   // inclusive prefix of list lengths over the batch
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -96,27 +106,20 @@ __device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - lb;
-        for (uint32_t base = 0; base < total; base += 64) {
-            uint32_t w[2];
-            bool ok[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const uint32_t pos = base + r * 32 + lane;
-                // largest segment q with excl_q <= pos
-                uint32_t lo = 0;
-#pragma unroll
-                for (int stp = 16; stp > 0; stp >>= 1) {
-                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + stp);
-                    if (ex <= pos) lo += stp;
-                }
-                const uint32_t sb = __shfl_sync(0xffffffffu, b0, lo);
-                const uint32_t se = __shfl_sync(0xffffffffu, excl, lo);
-                ok[r] = pos < total;
-                w[r] = ok[r] ? __ldg(Bc + sb + (pos - se)) : 0u;
+        __syncwarp();
+        if (lb > 0) scratch[__popc(nonempty & lt_mask)] = b0 - excl;
+        __syncwarp();
+        for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t in = excl - base;   // start offset of this lane's list in the round
+            const uint32_t bit = (lb > 0 && excl > base && in < 32u) ? (1u << in) : 0u;
+            const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+            const int cur = __popc(__ballot_sync(0xffffffffu, lb > 0 && excl <= base)) - 1;
+            const uint32_t pos = base + lane;
+            if (pos < total) {
+                const uint32_t seg = cur + __popc(starts & le_mask);
+                const uint32_t w = __ldg(Bc + (pos + scratch[seg]));
+                acc += probe<MODE>(S, w, hbits, hmask);
             }
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-                if (ok[r]) acc += probe<MODE>(S, w[r], hbits, hmask);
         }
     }
     return acc;
@@ -125,12 +128,21 @@ __device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol
 // Dense A_jx (bitmap rows of W words): |A_ix[u] ∩ A_jx[v]| = sum_k popc(S[k] & row_v[k]).
 // The warp is split into G = 32/gsz groups (gsz = pow2 >= W, capped at 32), one
 // v per group, so narrow parts keep every lane busy.
+// R = words of u's bitmap each lane keeps in registers (covers W <= 32*R);
+// R = 0: read them from shared memory (wide parts).
+template <int R>
 __device__ __forceinline__ uint32_t and_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                             const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
                                             int lane) {
     uint32_t gsz = 1;
     while (gsz < W && gsz < 32) gsz <<= 1;
     const uint32_t G = 32 / gsz, g = lane / gsz, kl = lane % gsz;
+    uint32_t su[R > 0 ? R : 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t k = kl + r * 32;
+        su[r] = (k < W) ? S[k] : 0u;
+    }
     uint32_t acc = 0;
     for (uint32_t e = e0; e < e1; e += 32) {
         const uint32_t nb = min(32u, e1 - e);
@@ -139,8 +151,14 @@ __device__ __forceinline__ uint32_t and_row(const uint32_t* __restrict__ vcol, u
             const uint32_t qq = q + g;
             const uint32_t vq = __shfl_sync(0xffffffffu, v, qq & 31);
             if (qq < nb) {
-                const uint32_t* __restrict__ row = BM + (uint64_t)vq * W;
-                for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + k));
+                const uint32_t* __restrict__ row = BM + (uint64_t)vq * W + kl;
+                if (R > 0) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (kl + r * 32 < W) acc += __popc(su[r] & __ldg(row + r * 32));
+                } else {
+                    for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + (k - kl)));
+                }
             }
         }
     }
@@ -155,12 +173,16 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* S = smem + wid * kSetWords;
+    uint32_t* S = smem + wid * (kSetWords + 32);
+    uint32_t* scratch = S + kSetWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     __syncwarp();
     const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
-    for (unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid; idx < nitems; idx += nwarps) {
-        const unsigned long long it = items[idx];
+    unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid;
+    unsigned long long it_next = (idx < nitems) ? __ldg(items + idx) : 0ull;
+    for (; idx < nitems; idx += nwarps) {
+        const unsigned long long it = it_next;
+        if (idx + nwarps < nitems) it_next = __ldg(items + idx + nwarps);   // prefetch the next item
         const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
         const TaskDev T = tasks[t];
         const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
@@ -182,9 +204,15 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
             }
             __syncwarp();
             if (T.bm_jx != ~0ull)
-                acc = and_row(vcol, e0, e1, bitmap + T.bm_jx, T.bm_words, S, lane);
+            {
+                const uint32_t* BM = bitmap + T.bm_jx;
+                const uint32_t W = T.bm_words;
+                if (W <= 32) acc = and_row<1>(vcol, e0, e1, BM, W, S, lane);
+                else if (W <= 128) acc = and_row<4>(vcol, e0, e1, BM, W, S, lane);
+                else acc = and_row<0>(vcol, e0, e1, BM, W, S, lane);
+            }
             else
-                acc = stream_row<0>(vcol, e0, e1, rp_jx, Bc, S, hbits, hmask, lane);
+                acc = stream_row<0>(vcol, e0, e1, rp_jx, Bc, S, scratch, hbits, hmask, lane);
             __syncwarp();
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
         } else if (mode == 1) {
@@ -194,7 +222,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
-            acc = stream_row<1>(vcol, e0, e1, rp_jx, Bc, S, hbits, hmask, lane);
+            acc = stream_row<1>(vcol, e0, e1, rp_jx, Bc, S, scratch, hbits, hmask, lane);
             __syncwarp();
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
@@ -205,8 +233,9 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
             }
         }
         __syncwarp();
-        const unsigned long long sum = warp_sum(acc);
-        if (lane == 0 && sum) atomicAdd(&task_counts[t], sum);
+        // a row's count is < 2^32 (<= |A_ix[u]| * |A_ij[u]|), so a 32-bit REDUX suffices
+        const uint32_t sum = __reduce_add_sync(0xffffffffu, acc);
+        if (lane == 0 && sum) atomicAdd(&task_counts[t], (unsigned long long)sum);
     }
 }
 
@@ -260,7 +289,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     PG_CK(cudaEventRecord(h->ev1, st));
     if (h->n_items) {
         static thread_local int cached_dev = -1, grid = 0;
-        const size_t smem = kRowWarps * kSetWords * sizeof(uint32_t);
+        const size_t smem = kRowWarps * (kSetWords + 32) * sizeof(uint32_t);
         if (cached_dev != h->device) {
             PG_CK(cudaFuncSetAttribute(k_tc_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int sms = 0, per_sm = 0;
