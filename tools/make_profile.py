@@ -1,0 +1,62 @@
+"""Collect one GPU call's evidence into profiles/: the bench line, the ncu launch
+list summary and the ncu --set full summary of k_tc_rows.
+
+    python tools/make_profile.py <tag> <config> [round]
+reads gpurun_out/{bench,launches,prof}_<tag>.* and writes profiles/r<round>_<tag>.json;
+also records the kernel's DRAM bytes per launch in profiles/ncu_summary.json
+(bench.py reports it as roofline.traffic for that config).
+"""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+
+from launch_summary import summarize  # noqa: E402
+from ncu_summary import summary  # noqa: E402
+
+
+def to_bytes(s):
+    v, u = s.split()
+    return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[u]
+
+
+def main(tag, config, rnd="01"):
+    g = os.path.join(ROOT, "gpurun_out")
+    out = {"tag": tag, "config": config}
+    bj = os.path.join(g, f"bench_{tag}.json")
+    if os.path.exists(bj):
+        lines = [ln for ln in open(bj) if ln.strip().startswith("{")]
+        out["bench"] = json.loads(lines[0]) if lines else None
+    lc = os.path.join(g, f"launches_{tag}.csv")
+    if os.path.exists(lc):
+        s = summarize(lc)
+        out["launches"] = {k: v for k, v in s.items() if k in ("k_tc_rows", "k_sum_tasks")}
+        out["launches_build_total_ms"] = sum(v["total_ms"] for k, v in s.items()
+                                             if k not in ("k_tc_rows", "k_sum_tasks"))
+        out["launches_note"] = ("ncu launch list (--metrics gpu__time_duration.sum --clock-control none): "
+                                "cold-cache, serialised; compare shares, not absolutes")
+    rep = os.path.join(g, f"prof_{tag}.ncu-rep")
+    if os.path.exists(rep):
+        ks = [d for d in summary(rep) if "k_tc_rows" in d["kernel"]]
+        if ks:
+            k = ks[0]
+            out["ncu_k_tc_rows"] = k
+            traffic = to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"])
+            out["dram_bytes_per_launch"] = traffic
+            ns = os.path.join(ROOT, "profiles", "ncu_summary.json")
+            js = json.load(open(ns)) if os.path.exists(ns) else {}
+            js[config] = {"dram_bytes_per_launch": traffic, "source": f"profiles/r{rnd}_{tag}.json",
+                          "l2_hit_pct": k.get("lts__t_sector_hit_rate.pct"),
+                          "kernel_ms_under_ncu": k.get("gpu__time_duration.sum")}
+            json.dump(js, open(ns, "w"), indent=1, sort_keys=True)
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    path = os.path.join(ROOT, "profiles", f"r{rnd}_{tag}.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print(path)
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
