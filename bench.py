@@ -187,18 +187,65 @@ def run_reference(args):
     return 0
 
 
+class Comm:
+    """Process-group plumbing for N>1: NCCL when every rank has its own GPU (the
+    production path: the 8-byte count allreduce runs on the GPU stream); gloo with
+    host tensors when ranks share a GPU (lets the multi-rank flow run on a 1-GPU box)."""
+
+    def __init__(self, ws, local):
+        import torch
+        import torch.distributed as dist
+        self.ws, self.dist, self.torch = ws, dist, torch
+        ndev = torch.cuda.device_count()
+        self.dev = local % max(ndev, 1)
+        torch.cuda.set_device(self.dev)
+        self.backend = None
+        if ws > 1:
+            self.backend = "nccl" if ndev >= ws else "gloo"
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.dev))
+            else:
+                dist.init_process_group("gloo")
+
+    def allreduce_(self, t, op="sum"):
+        if self.ws <= 1:
+            return t
+        dop = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
+        if self.backend == "nccl":
+            self.dist.all_reduce(t, op=dop)
+            return t
+        h = t.cpu()
+        self.dist.all_reduce(h, op=dop)
+        t.copy_(h)
+        return t
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def close(self):
+        if self.ws > 1:
+            self.dist.destroy_process_group()
+
+
+def golden_triangles(config):
+    """Oracle count written by tests/golden/make_golden.py (oracle-only script)."""
+    path = os.path.join(ROOT, "tests", "golden", "triangles.json")
+    try:
+        return json.load(open(path)).get(config, {}).get("triangles")
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     from gen.configs import CONFIGS
     import paper_2209_04541_b200 as pg
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.cuda.current_device()
+    comm = Comm(ws, local)
+    dev = comm.dev
     cfg = CONFIGS[args.config]
     p = args.p or cfg.p
     n, s, d = cfg.generate()
@@ -216,8 +263,7 @@ def run_ours(args):
 
     def step():
         b.triangle_count(stream=stream.cuda_stream, d_count=out.data_ptr(), sync=False)
-        if ws > 1:
-            dist.all_reduce(out)
+        comm.allreduce_(out)            # S11: one 8-byte allreduce of the per-rank counts
 
     for _ in range(args.warmup):
         step()
@@ -227,8 +273,7 @@ def run_ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kern_ms, launches = [], 0
     with ClockSampler(dev) as clk:
-        if ws > 1:
-            dist.barrier()
+        comm.barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
             flush.zero_()                       # L2 flush between timed steps (outside events)
@@ -240,14 +285,10 @@ def run_ours(args):
             kern_ms.append(stk["ms_main_kernel_last"])
             launches += int(stk["launches_last"])
         torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
+        comm.barrier()
     step_ms = [a.elapsed_time(z) for a, z in ev]
-    tot_ms = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    tot_ms = float(comm.allreduce_(tot, "max").item())       # max over ranks
     ms_per_step = tot_ms / args.steps
     value = m_edges / (ms_per_step / 1e3)
 
@@ -258,10 +299,11 @@ def run_ours(args):
     kms = statistics.mean(kern_ms) if kern_ms else float("nan")
     achieved = alg / (kms / 1e3) / 1e9 if kms > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.config),
-                "kernel": "k_tc_warp (S10 intersections)", "kernel_ms": kms,
+                "frac": achieved / peak, "traffic": load_traffic(args.config) if ws == 1 else None,
+                "kernel": "k_tc_rows (S10 intersections)", "kernel_ms": kms,
                 "kernel_share_of_step": kms / ms_per_step if ms_per_step else None,
-                "alg_bytes_per_launch": alg, "peak_source": peak_src}
+                "alg_bytes_per_launch": alg, "peak_source": peak_src,
+                "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19"}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
@@ -270,29 +312,24 @@ def run_ours(args):
                              residency=pg.RESIDENT_HOST)
         for _ in range(max(1, args.warmup)):
             bh.triangle_count()
-        if ws > 1:
-            dist.barrier()
+        comm.barrier()
         torch.cuda.synchronize()
         wall = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            local = bh.triangle_count()        # H2D of blocks + count + D2H of the count
-            if ws > 1:
-                tt = torch.tensor([local], dtype=torch.int64, device="cuda")
-                dist.all_reduce(tt)
-                tt.item()
+            local_T = bh.triangle_count()      # H2D of blocks + count + D2H of the count
+            tt = torch.tensor([local_T], dtype=torch.int64, device="cuda")
+            comm.allreduce_(tt)
+            tt.item()
             wall.append(time.perf_counter() - t0)
-        e_s = sum(wall)
-        if ws > 1:
-            t = torch.tensor([e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_s = float(t.item())
+        e_t = torch.tensor([sum(wall)], dtype=torch.float64, device="cuda")
+        e_s = float(comm.allreduce_(e_t, "max").item())
         sh = bh.stats()
         e2e = {"value": m_edges / (e_s / args.steps), "unit": UNIT,
                "h2d_bytes_per_step": int(sh["h2d_bytes_last"]), "d2h_bytes_per_step": 8,
-               "ms_per_step": 1e3 * e_s / args.steps}
+               "ms_per_step": 1e3 * e_s / args.steps, "timer": "host wall clock around the public call"}
         bh.free()
 
     cpu = None
@@ -308,6 +345,7 @@ def run_ours(args):
                        "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
                        "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
                        "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}",
+                       "comm": comm.backend,
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "timer": "CUDA events per step on the launch stream, max over ranks"},
             "roofline": roofline,
@@ -316,13 +354,16 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        gold = golden_triangles(args.config)
         if cpu and cpu.get("full"):
             line["parity"] = {"oracle_triangles": cpu["triangles_in_sample"],
-                              "match": cpu["triangles_in_sample"] == T}
+                              "match": cpu["triangles_in_sample"] == T, "source": "oracle run in this job"}
+        elif gold is not None:
+            line["parity"] = {"oracle_triangles": gold, "match": gold == T,
+                              "source": "tests/golden/triangles.json (oracle-only script)"}
         print(json.dumps(line), flush=True)
     b.free()
-    if ws > 1:
-        dist.destroy_process_group()
+    comm.close()
     return 0
 
 

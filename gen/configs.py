@@ -37,5 +37,7 @@ CONFIGS = {
     "c3": Config("c3", "Erdos-Renyi n=2^24, avg degree 32, 16x16 blocks", 16, "er", (1 << 24, 32, 1)),
     "c4": Config("c4", "grid 8192^2 + 10% diagonals (road-like), n=2^26, 16x16 blocks", 16, "grid",
                  (8192, 0.1, 1)),
+    # profiling stand-in for c5 (same generator and p at 1/4 of the vertices; ncu-sized)
+    "c5s": Config("c5s", "R-MAT scale 24, edge factor 32, 16x16 blocks", 16, "rmat", (24, 32, 1)),
     "c5": Config("c5", "Graph500 R-MAT scale 26, edge factor 32, 16x16 blocks", 16, "rmat", (26, 32, 1)),
 }

@@ -224,24 +224,41 @@ struct CostArg {
     unsigned long long* alg_el;
 };
 
-__global__ void k_task_costs(CostArg a) {
-    const uint64_t mask = (1ull << a.B) - 1;
+// Launched per non-empty block (i, j): every lane of a warp shares the block, so
+// the x-loop is warp-uniform and each (warp, task) adds one warp-reduced sum.
+__global__ void k_task_costs(CostArg a, int i, int j) {
+    const BlockDev bij = a.blk[i * a.p + j];
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < a.mE; k += stride) {
-        const uint64_t key = a.dag[k];
-        const uint32_t r = (uint32_t)(key >> a.B), c = (uint32_t)(key & mask);
-        const int i = part_of(a.cu, r), j = part_of(a.cu, c);
-        const uint32_t u = r - a.cu.c[i], v = c - a.cu.c[j];
-        const BlockDev bij = a.blk[i * a.p + j];
-        const bool first = (k == bij.col_off) || ((a.dag[k - 1] >> a.B) != r);
+    for (uint64_t base = warp0; base < bij.nnz; base += stride) {
+        const uint64_t k = bij.col_off + base + lane;
+        const bool ok = base + lane < bij.nnz;
+        uint32_t u = 0, v = 0;
+        bool first = false;
+        if (ok) {
+            const uint32_t r = (uint32_t)(a.dag[k] >> a.B);
+            u = r - a.cu.c[i];
+            v = a.col[k];
+            first = (k == bij.col_off) || ((uint32_t)(a.dag[k - 1] >> a.B) != r);
+        }
         for (int x = j; x < a.p; ++x) {
             const uint32_t t = a.tid[(i * a.p + j) * a.p + x];
             if (t == kNoTask) continue;
-            const BlockDev bix = a.blk[i * a.p + x], bjx = a.blk[j * a.p + x];
-            const uint32_t la = a.rowptr[bix.rp_off + u + 1] - a.rowptr[bix.rp_off + u];
-            const uint32_t lb = a.rowptr[bjx.rp_off + v + 1] - a.rowptr[bjx.rp_off + v];
-            atomicAdd(&a.cost[t], (unsigned long long)(la + lb));
-            atomicAdd(&a.alg_el[t], (unsigned long long)(lb + (first ? la : 0u)));
+            uint32_t c = 0, el = 0;
+            if (ok) {
+                const BlockDev bix = a.blk[i * a.p + x], bjx = a.blk[j * a.p + x];
+                const uint32_t la = a.rowptr[bix.rp_off + u + 1] - a.rowptr[bix.rp_off + u];
+                const uint32_t lb = a.rowptr[bjx.rp_off + v + 1] - a.rowptr[bjx.rp_off + v];
+                c = la + lb;
+                el = lb + (first ? la : 0u);
+            }
+            c = __reduce_add_sync(0xffffffffu, c);
+            el = __reduce_add_sync(0xffffffffu, el);
+            if (lane == 0) {
+                atomicAdd(&a.cost[t], (unsigned long long)c);
+                atomicAdd(&a.alg_el[t], (unsigned long long)el);
+            }
         }
     }
 }
@@ -279,27 +296,25 @@ __global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsig
 }
 
 // Row items of one owned piece: rows u in [r0, r1) with A_ij[u] and A_ix[u]
-// non-empty, with their estimated work |A_ix[u]| + sum_v |A_jx[v]| (the staged
-// model's element count for the row).  out == nullptr: count only.
-__global__ void k_row_items(PieceDev w, const uint32_t* col, const uint32_t* rowptr, unsigned long long* out,
-                            uint32_t* out_work, unsigned long long* counter) {
-    for (uint64_t r = w.r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < w.r1;
-         r += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = (uint32_t)r;
-        const uint32_t e0 = rowptr[w.rp_ij + u], e1 = rowptr[w.rp_ij + u + 1];
-        if (e0 == e1) continue;
-        const uint32_t la = rowptr[w.rp_ix + u + 1] - rowptr[w.rp_ix + u];
-        if (la == 0) continue;
-        const unsigned long long idx = atomicAdd(counter, 1ull);
-        if (!out) continue;
-        unsigned long long work = la;
-        for (uint32_t e = e0; e < e1; ++e) {
-            const uint32_t v = col[w.col_ij + e];
-            work += rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v];
+// non-empty.  flags[r - r0] = 1 for those rows (flags[nrows] = 0 for the scan).
+__global__ void k_row_flags(PieceDev w, const uint32_t* rowptr, uint32_t* flags) {
+    const uint32_t nr = w.r1 - w.r0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= nr;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t f = 0;
+        if (k < nr) {
+            const uint32_t u = w.r0 + (uint32_t)k;
+            f = (rowptr[w.rp_ij + u + 1] > rowptr[w.rp_ij + u]) && (rowptr[w.rp_ix + u + 1] > rowptr[w.rp_ix + u]);
         }
-        out[idx] = ((unsigned long long)w.task << 32) | u;
-        out_work[idx] = (uint32_t)min(work, 0xffffffffull);
+        flags[k] = f;
     }
+}
+
+__global__ void k_row_emit(PieceDev w, const uint32_t* flags, const uint32_t* pos, unsigned long long* out) {
+    const uint32_t nr = w.r1 - w.r0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nr;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        if (flags[k]) out[pos[k]] = ((unsigned long long)w.task << 32) | (w.r0 + (uint32_t)k);
 }
 
 template <class F>
@@ -590,8 +605,13 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         CostArg a;
         a.dag = dag; a.col = h->d_col.p; a.rowptr = h->d_rowptr.p; a.blk = d_blk.p; a.tid = d_tid.p;
         a.B = B; a.p = (int)p; a.cu = cu; a.mE = mE; a.cost = d_cost.p; a.alg_el = d_alg.p;
-        k_task_costs<<<grid_for(mE), kThreads, 0, st>>>(a);
-        PG_LAUNCH_CHECK();
+        for (uint32_t i = 0; i < p; ++i)
+            for (uint32_t j = i; j < p; ++j) {
+                const BlockInfo& b = h->blocks[i * p + j];
+                if (!b.present) continue;
+                k_task_costs<<<grid_for(b.nnz), kThreads, 0, st>>>(a, (int)i, (int)j);
+                PG_LAUNCH_CHECK();
+            }
         std::vector<unsigned long long> c(nt), ae(nt);
         PG_CK(cudaMemcpyAsync(c.data(), d_cost.p, nt * 8, cudaMemcpyDeviceToHost, st));
         PG_CK(cudaMemcpyAsync(ae.data(), d_alg.p, nt * 8, cudaMemcpyDeviceToHost, st));
@@ -745,41 +765,62 @@ void upload_work(pgabb_blocks_s* h) {
     h->d_tasks.alloc(td.size());
     PG_CK(cudaMemcpy(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
 
-    // row items of the owned pieces, heaviest first (in-GPU analogue of the paper's
-    // "sorts them in decreasing order")
+    // Row items of the owned pieces, laid out for L2 locality: pieces in task
+    // order (x desc, j desc, i asc) so that the warps running concurrently share
+    // the v-side block A_jx (and the hub column part is done first), rows
+    // ascending inside a piece.  Compaction is a flag + exclusive scan per piece,
+    // so the layout is deterministic.
     cudaStream_t st = h->stream;
-    DBuf<unsigned long long> cnt;
-    cnt.alloc(1);
-    PG_CK(cudaMemsetAsync(cnt.p, 0, 8, st));
-    for (const PieceDev& w : h->work) {
-        k_row_items<<<grid_for(w.r1 - w.r0), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, nullptr, nullptr,
-                                                                 cnt.p);
+    std::vector<size_t> order(h->work.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        const Task &A = h->tasks[h->work[a].task], &Bt = h->tasks[h->work[b].task];
+        if (A.x != Bt.x) return A.x > Bt.x;
+        if (A.j != Bt.j) return A.j > Bt.j;
+        if (A.i != Bt.i) return A.i < Bt.i;
+        return h->work[a].r0 < h->work[b].r0;
+    });
+    uint32_t maxrows = 0;
+    for (const PieceDev& w : h->work) maxrows = std::max(maxrows, w.r1 - w.r0);
+    DBuf<uint32_t> flags, pos;
+    DBuf<unsigned char> tmp;
+    flags.alloc((size_t)maxrows + 1);
+    pos.alloc((size_t)maxrows + 1);
+    std::vector<uint64_t> piece_items(h->work.size(), 0);
+    // pass 1: count per piece
+    for (size_t k : order) {
+        const PieceDev& w = h->work[k];
+        const uint32_t nr = w.r1 - w.r0;
+        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_rowptr.p, flags.p);
         PG_LAUNCH_CHECK();
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(tp, b, flags.p, pos.p, (int64_t)nr + 1, st);
+        }, st, tmp);
+        uint32_t cntp = 0;
+        PG_CK(cudaMemcpyAsync(&cntp, pos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaStreamSynchronize(st));
+        piece_items[k] = cntp;
     }
-    unsigned long long nitems = 0;
-    PG_CK(cudaMemcpyAsync(&nitems, cnt.p, 8, cudaMemcpyDeviceToHost, st));
-    PG_CK(cudaStreamSynchronize(st));
+    uint64_t nitems = 0;
+    for (uint64_t c : piece_items) nitems += c;
     h->n_items = nitems;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
-    if (nitems) {
-        DBuf<unsigned long long> items;
-        DBuf<uint32_t> wk, wk2;
-        DBuf<unsigned char> tmp;
-        items.alloc(nitems);
-        wk.alloc(nitems);
-        wk2.alloc(nitems);
-        PG_CK(cudaMemsetAsync(cnt.p, 0, 8, st));
-        for (const PieceDev& w : h->work) {
-            k_row_items<<<grid_for(w.r1 - w.r0), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, items.p, wk.p,
-                                                                     cnt.p);
-            PG_LAUNCH_CHECK();
-        }
+    // pass 2: emit in layout order
+    uint64_t base = 0;
+    for (size_t k : order) {
+        const PieceDev& w = h->work[k];
+        const uint32_t nr = w.r1 - w.r0;
+        if (!piece_items[k]) continue;
+        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_rowptr.p, flags.p);
+        PG_LAUNCH_CHECK();
         cub_call([&](void* tp, size_t& b) {
-            return cub::DeviceRadixSort::SortPairsDescending(tp, b, wk.p, wk2.p, items.p, h->d_items.p,
-                                                             (int64_t)nitems, 0, 32, st);
+            return cub::DeviceScan::ExclusiveSum(tp, b, flags.p, pos.p, (int64_t)nr + 1, st);
         }, st, tmp);
-        PG_CK(cudaStreamSynchronize(st));
+        k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, flags.p, pos.p, h->d_items.p + base);
+        PG_LAUNCH_CHECK();
+        base += piece_items[k];
     }
+    PG_CK(cudaStreamSynchronize(st));
 }
 
 }  // namespace pgabb

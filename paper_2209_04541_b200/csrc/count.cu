@@ -74,28 +74,113 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
     return s == w + 1;
 }
 
-// Stream the lists of A_jx[v] for v in A_ij[u] (edges e0..e1) against the set S.
-// The non-empty lists of a batch of 32 v are compacted (ballot + popc) and their
-// "index delta" (list start - flattened start) parked in 32 words of warp
-// scratch; in each round of 32 flattened positions, the segment of position
-// base+l is cur + popc(starts in (base, base+l]), where the start mask comes from
+// One row u: every v in A_ij[u] (edges e0..e1), 32 at a time (one per lane).
+//
+// List pairs: the non-empty lists of the batch are one flattened sequence;
+// their "index delta" (list start - flattened start) is parked in warp scratch
+// by compacted index (ballot + popc); in each round of 32 positions the list of
+// position base+l is cur + popc(starts in (base, base+l]), the start mask from
 // one __reduce_or_sync and cur from one ballot -- no per-position search.
-template <int MODE>
-__device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
-                                               const uint32_t* __restrict__ rp_jx,
-                                               const uint32_t* __restrict__ Bc, const uint32_t* S,
-                                               uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
-                                               int lane) {
+// Elements probe the staged set S (MODE 0 bitmap, 1 hash).
+//
+// Dense pairs (A_jx has a bitmap copy BM with W words per row, and v's list is
+// longer than W): |A_ix[u] ∩ A_jx[v]| = sum_k popc(S[k] & row_v[k]); the warp is
+// split into G = 32/gsz groups (gsz = pow2 >= W, capped at 32), one v per group;
+// u's words are held in registers when W <= 32*R (R = 0: read from S).
+//
+// Skewed pairs (|A_ix[u]| * log2|A_jx[v]| * 6 < |A_jx[v]|: a short u list against
+// a long v list): thread per pair -- the lane binary-searches each element of
+// A_ix[u] (broadcast by shuffle, ascending, so the search window only shrinks)
+// in v's sorted list instead of streaming the whole list.
+__device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+template <int MODE, int R>
+__device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
+                                                  const uint32_t* __restrict__ rp_jx,
+                                                  const uint32_t* __restrict__ Bc,
+                                                  const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
+                                                  uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
+                                                  const uint32_t* __restrict__ A, uint32_t la, int lane) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t le_mask = 0xffffffffu >> (31 - lane);
+    uint32_t gsz = 1;
+    while (gsz < W && gsz < 32) gsz <<= 1;
+    const uint32_t G = 32 / gsz, g = lane / gsz, kl = lane % gsz;
+    uint32_t su[R > 0 ? R : 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t k = kl + r * 32;
+        su[r] = (BM != nullptr && k < W) ? S[k] : 0u;
+    }
     uint32_t acc = 0;
     for (uint32_t e = e0; e < e1; e += 32) {
-        uint32_t b0 = 0, lb = 0;
+        uint32_t v = 0, b0 = 0, lb = 0;
         if (e + lane < e1) {
-            const uint32_t v = __ldg(vcol + e + lane);
+            v = __ldg(vcol + e + lane);
             b0 = __ldg(rp_jx + v);
             lb = __ldg(rp_jx + v + 1) - b0;
         }
+        // dense pairs: AND of bitmap rows
+        const bool use_and = (BM != nullptr) && lb > W;
+        const uint32_t and_mask = __ballot_sync(0xffffffffu, use_and);
+        if (and_mask) {
+            __syncwarp();
+            if (use_and) scratch[32 + __popc(and_mask & lt_mask)] = v;
+            __syncwarp();
+            const uint32_t na = __popc(and_mask);
+            for (uint32_t q = 0; q < na; q += G) {
+                const uint32_t qq = q + g;
+                if (qq < na) {
+                    const uint32_t* __restrict__ row = BM + (uint64_t)scratch[32 + qq] * W + kl;
+                    if (R > 0) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (kl + r * 32 < W) acc += __popc(su[r] & __ldg(row + r * 32));
+                    } else {
+                        for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + (k - kl)));
+                    }
+                }
+            }
+            if (use_and) lb = 0;
+        }
+        // skewed pairs: binary search of u's elements in v's list
+        const bool use_search = lb > 0 && la * log2ceil(lb + 1) * 6u < lb;
+        if (__any_sync(0xffffffffu, use_search)) {
+            uint32_t lo = 0;
+            for (uint32_t c = 0; c < la; c += 32) {
+                const uint32_t a = (c + lane < la) ? __ldg(A + c + lane) : 0u;
+                const uint32_t m = min(32u, la - c);
+                for (uint32_t k = 0; k < m; ++k) {
+                    const uint32_t ak = __shfl_sync(0xffffffffu, a, k);
+                    if (use_search) {
+                        uint32_t hi = lb;
+                        while (lo < hi) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (__ldg(Bc + b0 + mid) < ak) lo = mid + 1; else hi = mid;
+                        }
+                        acc += (lo < lb && __ldg(Bc + b0 + lo) == ak);
+                    }
+                }
+            }
+            if (use_search) lb = 0;
+        }
+        // long lists: one at a time, lanes striding through it (no segment math)
+        uint32_t long_mask = __ballot_sync(0xffffffffu, lb >= 64);
+        while (long_mask) {
+            const int q = __ffs(long_mask) - 1;
+            long_mask &= long_mask - 1;
+            const uint32_t qb0 = __shfl_sync(0xffffffffu, b0, q);
+            const uint32_t qlb = __shfl_sync(0xffffffffu, lb, q);
+            const uint32_t* __restrict__ L = Bc + qb0;
+            uint32_t k = lane;
+            for (; k + 32 < qlb; k += 64) {
+                const uint32_t w0 = __ldg(L + k), w1 = __ldg(L + k + 32);
+                acc += probe<MODE>(S, w0, hbits, hmask) + probe<MODE>(S, w1, hbits, hmask);
+            }
+            if (k < qlb) acc += probe<MODE>(S, __ldg(L + k), hbits, hmask);
+        }
+        if (lb >= 64) lb = 0;
+        // short lists: flattened probing
         const uint32_t nonempty = __ballot_sync(0xffffffffu, lb > 0);
         if (nonempty == 0u) continue;
         uint32_t incl = lb;   // inclusive prefix of list lengths over the batch
@@ -125,40 +210,24 @@ __device__ __forceinline__ uint32_t stream_row(const uint32_t* __restrict__ vcol
     return acc;
 }
 
-// Dense A_jx (bitmap rows of W words): |A_ix[u] ∩ A_jx[v]| = sum_k popc(S[k] & row_v[k]).
-// The warp is split into G = 32/gsz groups (gsz = pow2 >= W, capped at 32), one
-// v per group, so narrow parts keep every lane busy.
-// R = words of u's bitmap each lane keeps in registers (covers W <= 32*R);
-// R = 0: read them from shared memory (wide parts).
-template <int R>
-__device__ __forceinline__ uint32_t and_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
-                                            const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
-                                            int lane) {
-    uint32_t gsz = 1;
-    while (gsz < W && gsz < 32) gsz <<= 1;
-    const uint32_t G = 32 / gsz, g = lane / gsz, kl = lane % gsz;
-    uint32_t su[R > 0 ? R : 1];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const uint32_t k = kl + r * 32;
-        su[r] = (k < W) ? S[k] : 0u;
-    }
+// Dense A_jx and a short A_ix[u] (|A_ix[u]| <= 2W): thread per pair -- lane l
+// takes v_l and tests each element a of A_ix[u] (broadcast by shuffle) against
+// bit a of v_l's bitmap row.  Costs |A_ix[u]| bit tests per pair instead of W
+// word ANDs, and needs no staging of u at all.
+__device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
+                                                    const uint32_t* __restrict__ A, uint32_t la,
+                                                    const uint32_t* __restrict__ BM, uint32_t W, int lane) {
     uint32_t acc = 0;
     for (uint32_t e = e0; e < e1; e += 32) {
-        const uint32_t nb = min(32u, e1 - e);
-        const uint32_t v = ((uint32_t)lane < nb) ? __ldg(vcol + e + lane) : 0u;
-        for (uint32_t q = 0; q < nb; q += G) {
-            const uint32_t qq = q + g;
-            const uint32_t vq = __shfl_sync(0xffffffffu, v, qq & 31);
-            if (qq < nb) {
-                const uint32_t* __restrict__ row = BM + (uint64_t)vq * W + kl;
-                if (R > 0) {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (kl + r * 32 < W) acc += __popc(su[r] & __ldg(row + r * 32));
-                } else {
-                    for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + (k - kl)));
-                }
+        const bool ok = e + lane < e1;
+        const uint32_t v = ok ? __ldg(vcol + e + lane) : 0u;
+        const uint32_t* __restrict__ row = BM + (uint64_t)v * W;
+        for (uint32_t c = 0; c < la; c += 32) {
+            const uint32_t a = (c + lane < la) ? __ldg(A + c + lane) : 0u;
+            const uint32_t m = min(32u, la - c);
+            for (uint32_t k = 0; k < m; ++k) {
+                const uint32_t ak = __shfl_sync(0xffffffffu, a, k);
+                if (ok) acc += (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u;
             }
         }
     }
@@ -173,7 +242,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* S = smem + wid * (kSetWords + 32);
+    uint32_t* S = smem + wid * (kSetWords + 64);
     uint32_t* scratch = S + kSetWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     __syncwarp();
@@ -197,22 +266,23 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
         while ((1u << hbits) < 2 * la) ++hbits;
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
-        if (mode == 0) {
+        if (T.bm_jx != ~0ull && la <= 2 * T.bm_words) {
+            acc = probe_dense_row(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane);
+        } else if (mode == 0) {
             for (uint32_t k = lane; k < la; k += 32) {
                 const uint32_t w = __ldg(A + k);
                 atomicOr(&S[w >> 5], 1u << (w & 31));
             }
             __syncwarp();
-            if (T.bm_jx != ~0ull)
-            {
+            if (T.bm_jx != ~0ull) {
                 const uint32_t* BM = bitmap + T.bm_jx;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = and_row<1>(vcol, e0, e1, BM, W, S, lane);
-                else if (W <= 128) acc = and_row<4>(vcol, e0, e1, BM, W, S, lane);
-                else acc = and_row<0>(vcol, e0, e1, BM, W, S, lane);
+                if (W <= 32) acc = intersect_row<0, 1>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
+                else if (W <= 128) acc = intersect_row<0, 4>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
+                else acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
+            } else {
+                acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane);
             }
-            else
-                acc = stream_row<0>(vcol, e0, e1, rp_jx, Bc, S, scratch, hbits, hmask, lane);
             __syncwarp();
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
         } else if (mode == 1) {
@@ -222,7 +292,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
-            acc = stream_row<1>(vcol, e0, e1, rp_jx, Bc, S, scratch, hbits, hmask, lane);
+            acc = intersect_row<1, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane);
             __syncwarp();
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
@@ -289,7 +359,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     PG_CK(cudaEventRecord(h->ev1, st));
     if (h->n_items) {
         static thread_local int cached_dev = -1, grid = 0;
-        const size_t smem = kRowWarps * (kSetWords + 32) * sizeof(uint32_t);
+        const size_t smem = kRowWarps * (kSetWords + 64) * sizeof(uint32_t);
         if (cached_dev != h->device) {
             PG_CK(cudaFuncSetAttribute(k_tc_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int sms = 0, per_sm = 0;
