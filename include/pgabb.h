@@ -131,7 +131,9 @@ typedef struct {
     uint64_t block_bytes;               /* bytes of block CSR (all blocks) */
     uint64_t h2d_bytes_last;            /* host->device bytes of the last count call */
     uint64_t launches_last;             /* kernels launched by the last count call */
-    uint64_t reserved[4];
+    uint64_t waves;                     /* streaming residency: waves per count (0 otherwise) */
+    uint64_t max_task_bytes;            /* largest block-triple footprint (col+rowptr+dense copy) */
+    uint64_t reserved[2];
     double ms_build;                    /* wall time of pgabb_build_blocks */
     double ms_count_last;               /* device time of the last count call (events) */
     double ms_main_kernel_last;         /* device time of the intersection kernels */

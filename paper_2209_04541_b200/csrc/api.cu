@@ -66,6 +66,13 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     h_col.release();
     h_rowptr.release();
     h_bitmap.release();
+    d_wave_pieces.release();
+    d_wave_tasks.release();
+    d_arena[0].release();
+    d_arena[1].release();
+    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_done[0], ev_done[1]})
+        if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     d_bitmap.release();
     d_tasks.release();
     d_items.release();
@@ -130,9 +137,18 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->world_size = o.world_size;
         h->residency = o.residency;
         h->budget = o.device_budget_bytes;
+        h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
         build_graph(h, m, src, dst, o.inputs_on_device != 0);
         plan_pieces(h);
         upload_work(h);
+        if (h->streaming) {
+            plan_waves(h);
+            PG_CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+            for (int a = 0; a < 2; ++a) {
+                PG_CK(cudaEventCreateWithFlags(&h->ev_copied[a], cudaEventDisableTiming));
+                PG_CK(cudaEventCreateWithFlags(&h->ev_done[a], cudaEventDisableTiming));
+            }
+        }
         if (h->residency == PGABB_RESIDENT_HOST) {
             h->h_col.alloc(h->d_col.n);
             h->h_rowptr.alloc(h->d_rowptr.n);
@@ -142,6 +158,11 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
             h->h_bitmap.alloc(h->d_bitmap.n);
             if (h->d_bitmap.n)
                 PG_CK(cudaMemcpy(h->h_bitmap.p, h->d_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyDeviceToHost));
+            if (h->streaming) {   // the graph now lives in pinned host DRAM only
+                h->d_col.release();
+                h->d_rowptr.release();
+                h->d_bitmap.release();
+            }
         }
         PG_CK(cudaStreamSynchronize(h->stream));
         h->ms_build = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -186,6 +207,8 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->block_bytes = b->d_col.bytes() + b->d_rowptr.bytes() + b->d_bitmap.bytes();
         s->h2d_bytes_last = b->h2d_last;
         s->launches_last = b->launches_last;
+        s->waves = b->waves.size();
+        s->max_task_bytes = b->max_task_bytes;
         s->ms_build = b->ms_build;
         s->ms_count_last = b->ms_count_last;
         s->ms_main_kernel_last = b->ms_main_last;
@@ -215,14 +238,16 @@ pgabb_status_t pgabb_get_block(pgabb_blocks_t b, uint32_t i, uint32_t j, uint32_
         DeviceGuard g(b->device);
         const BlockInfo& bi = b->blocks[(size_t)i * b->p + j];
         *nnz = bi.nnz;
+        // streaming handles keep the pools in pinned host memory only
+        const uint32_t* rp_pool = b->d_rowptr.p ? b->d_rowptr.p : b->h_rowptr.p;
+        const uint32_t* col_pool = b->d_col.p ? b->d_col.p : b->h_col.p;
         if (rowptr) {
             if (bi.present)
-                PG_CK(cudaMemcpy(rowptr, b->d_rowptr.p + bi.rp_off, ((size_t)bi.nrows + 1) * 4, cudaMemcpyDeviceToHost));
+                PG_CK(cudaMemcpy(rowptr, rp_pool + bi.rp_off, ((size_t)bi.nrows + 1) * 4, cudaMemcpyDefault));
             else
                 std::memset(rowptr, 0, ((size_t)bi.nrows + 1) * 4);
         }
-        if (col && bi.nnz)
-            PG_CK(cudaMemcpy(col, b->d_col.p + bi.col_off, bi.nnz * 4, cudaMemcpyDeviceToHost));
+        if (col && bi.nnz) PG_CK(cudaMemcpy(col, col_pool + bi.col_off, bi.nnz * 4, cudaMemcpyDefault));
     });
 }
 

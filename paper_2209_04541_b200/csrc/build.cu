@@ -16,8 +16,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <numeric>
 #include <queue>
+#include <set>
 
 #include "internal.h"
 
@@ -701,6 +703,110 @@ void plan_pieces(pgabb_blocks_s* h) {
     }
 }
 
+// Owned pieces in execution order: task (x desc, j desc, i asc), then rows.
+static std::vector<size_t> locality_order(const pgabb_blocks_s* h) {
+    std::vector<size_t> order(h->work.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        const Task &A = h->tasks[h->work[a].task], &Bt = h->tasks[h->work[b].task];
+        if (A.x != Bt.x) return A.x > Bt.x;
+        if (A.j != Bt.j) return A.j > Bt.j;
+        if (A.i != Bt.i) return A.i < Bt.i;
+        return h->work[a].r0 < h->work[b].r0;
+    });
+    return order;
+}
+
+// Streaming residency: cut the owned pieces (in execution order) into waves whose
+// blocks fit half the device budget; each wave gets arena offsets for its blocks
+// and its own task-descriptor table.  EBUDGET if one task's three blocks alone
+// exceed half the budget ("hard error").
+void plan_waves(pgabb_blocks_s* h) {
+    const uint32_t p = h->p;
+    const uint64_t half = h->budget / 2 / 4;   // words per arena
+    const size_t nt = h->tasks.size();
+    h->waves.clear();
+    std::vector<WavePiece> wpieces;
+    std::vector<TaskDev> wtasks;
+    const std::vector<size_t> order = locality_order(h);
+    auto block_words = [&](uint32_t b, int pool) -> uint64_t {
+        const BlockInfo& B = h->blocks[b];
+        if (pool == 0) return B.nnz;
+        if (pool == 1) return (uint64_t)B.nrows + 1;
+        return B.bm_off == ~0ull ? 0 : (uint64_t)B.nrows * B.bm_words;
+    };
+    struct Need { uint32_t b; int pool; };
+    std::map<std::pair<uint32_t, int>, uint64_t> placed;   // (block, pool) -> arena word offset
+    Wave cur;
+    std::vector<TaskDev> cur_tasks;
+    auto open_wave = [&]() {
+        cur = Wave{};
+        cur.piece_begin = wpieces.size();
+        placed.clear();
+        cur_tasks.assign(nt, TaskDev{});
+    };
+    auto close_wave = [&]() {
+        if (cur.rows == 0) return;
+        cur.piece_end = wpieces.size();
+        cur.task_table = h->waves.size();
+        wtasks.insert(wtasks.end(), cur_tasks.begin(), cur_tasks.end());
+        h->waves.push_back(cur);
+    };
+    open_wave();
+    for (size_t k : order) {
+        const PieceDev& w = h->work[k];
+        const Task& T = h->tasks[w.task];
+        const uint32_t bij = T.i * p + T.j, bix = T.i * p + T.x, bjx = T.j * p + T.x;
+        std::vector<Need> need = {{bij, 0}, {bij, 1}, {bix, 0}, {bix, 1}, {bjx, 0}, {bjx, 1}, {bjx, 2}};
+        uint64_t all = 0, fresh = 0;
+        std::set<std::pair<uint32_t, int>> uniq;
+        for (const Need& q : need) {
+            if (!uniq.insert({q.b, q.pool}).second) continue;
+            const uint64_t wd = block_words(q.b, q.pool);
+            all += wd;
+            if (!placed.count({q.b, q.pool})) fresh += wd;
+        }
+        if (all > half)
+            fail(PGABB_EBUDGET, "task (" + std::to_string(T.i) + "," + std::to_string(T.j) + "," +
+                                    std::to_string(T.x) + ") needs " + std::to_string(all * 4) +
+                                    " bytes of blocks, more than half the device budget");
+        if (cur.words + fresh > half) {
+            close_wave();
+            open_wave();
+        }
+        for (const auto& key : uniq) {
+            if (placed.count(key)) continue;
+            const uint64_t wd = block_words(key.first, key.second);
+            const BlockInfo& B = h->blocks[key.first];
+            const uint64_t src = key.second == 0 ? B.col_off : key.second == 1 ? B.rp_off : B.bm_off;
+            placed[key] = cur.words;
+            if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, key.second});
+            cur.words += wd;
+        }
+        TaskDev d{};
+        d.col_ij = placed[{bij, 0}]; d.rp_ij = placed[{bij, 1}];
+        d.col_ix = placed[{bix, 0}]; d.rp_ix = placed[{bix, 1}];
+        d.col_jx = placed[{bjx, 0}]; d.rp_jx = placed[{bjx, 1}];
+        d.bm_jx = h->blocks[bjx].bm_off == ~0ull ? ~0ull : placed[{bjx, 2}];
+        d.bm_words = h->blocks[bjx].bm_words;
+        d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
+        cur_tasks[w.task] = d;
+        wpieces.push_back(WavePiece{cur.rows, w.task, w.r0});
+        cur.rows += w.r1 - w.r0;
+    }
+    close_wave();
+    h->d_wave_pieces.alloc(std::max<size_t>(wpieces.size(), 1));
+    if (!wpieces.empty())
+        PG_CK(cudaMemcpy(h->d_wave_pieces.p, wpieces.data(), wpieces.size() * sizeof(WavePiece),
+                         cudaMemcpyHostToDevice));
+    h->d_wave_tasks.alloc(std::max<size_t>(wtasks.size(), 1));
+    if (!wtasks.empty())
+        PG_CK(cudaMemcpy(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
+    uint64_t maxw = 1;
+    for (const Wave& wv : h->waves) maxw = std::max(maxw, wv.words);
+    for (int a = 0; a < 2; ++a) h->d_arena[a].alloc(maxw);
+}
+
 // This rank's work list: owned pieces in (task, row) order with their pool offsets.
 void upload_work(pgabb_blocks_s* h) {
     const uint32_t p = h->p;
@@ -765,21 +871,31 @@ void upload_work(pgabb_blocks_s* h) {
     h->d_tasks.alloc(td.size());
     PG_CK(cudaMemcpy(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
 
+    // largest block-triple footprint (what one task needs resident, S9)
+    h->max_task_bytes = 0;
+    for (const Task& T : h->tasks) {
+        const uint32_t ids[3] = {T.i * p + T.j, T.i * p + T.x, T.j * p + T.x};
+        uint64_t bytes = 0;
+        for (int a = 0; a < 3; ++a) {
+            bool dup = false;
+            for (int z = 0; z < a; ++z) dup |= (ids[z] == ids[a]);
+            if (dup) continue;
+            const BlockInfo& B = h->blocks[ids[a]];
+            bytes += 4 * (B.nnz + (uint64_t)B.nrows + 1);
+        }
+        const BlockInfo& J = h->blocks[ids[2]];
+        if (J.bm_off != ~0ull) bytes += 4ull * J.nrows * J.bm_words;
+        h->max_task_bytes = std::max(h->max_task_bytes, bytes);
+    }
+    if (h->streaming) return;   // streaming residency enumerates rows implicitly per wave
+
     // Row items of the owned pieces, laid out for L2 locality: pieces in task
     // order (x desc, j desc, i asc) so that the warps running concurrently share
     // the v-side block A_jx (and the hub column part is done first), rows
     // ascending inside a piece.  Compaction is a flag + exclusive scan per piece,
     // so the layout is deterministic.
     cudaStream_t st = h->stream;
-    std::vector<size_t> order(h->work.size());
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
-        const Task &A = h->tasks[h->work[a].task], &Bt = h->tasks[h->work[b].task];
-        if (A.x != Bt.x) return A.x > Bt.x;
-        if (A.j != Bt.j) return A.j > Bt.j;
-        if (A.i != Bt.i) return A.i < Bt.i;
-        return h->work[a].r0 < h->work[b].r0;
-    });
+    const std::vector<size_t> order = locality_order(h);
     uint32_t maxrows = 0;
     for (const PieceDev& w : h->work) maxrows = std::max(maxrows, w.r1 - w.r0);
     DBuf<uint32_t> flags, pos;

@@ -234,9 +234,14 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
     return acc;
 }
 
+// IMPLICIT = false: items[] holds the compacted row items (device-resident blocks).
+// IMPLICIT = true (streaming residency): item idx is row idx of the wave's piece
+// table wp[0..nwp) (rows of empty lists are skipped in the kernel), and the pool
+// pointers all point at the wave's staging arena.
+template <bool IMPLICIT>
 __global__ void __launch_bounds__(kRowWarps * 32)
-k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitems,
-          const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
+k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
+          unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
           unsigned long long* __restrict__ task_counts) {
     extern __shared__ uint32_t smem[];
@@ -248,15 +253,28 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     __syncwarp();
     const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
     unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid;
-    unsigned long long it_next = (idx < nitems) ? __ldg(items + idx) : 0ull;
+    unsigned long long it_next = (!IMPLICIT && idx < nitems) ? __ldg(items + idx) : 0ull;
     for (; idx < nitems; idx += nwarps) {
-        const unsigned long long it = it_next;
-        if (idx + nwarps < nitems) it_next = __ldg(items + idx + nwarps);   // prefetch the next item
-        const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
+        uint32_t t, u;
+        if (IMPLICIT) {
+            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
+            }
+            t = wp[lo].task;
+            u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
+        } else {
+            const unsigned long long it = it_next;
+            if (idx + nwarps < nitems) it_next = __ldg(items + idx + nwarps);   // prefetch the next item
+            t = (uint32_t)(it >> 32);
+            u = (uint32_t)it;
+        }
         const TaskDev T = tasks[t];
         const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
         const uint32_t e0 = __ldg(rowptr + T.rp_ij + u), e1 = __ldg(rowptr + T.rp_ij + u + 1);
         const uint32_t la = a1 - a0;
+        if (IMPLICIT && (la == 0 || e1 == e0)) continue;
         const uint32_t* __restrict__ A = col + T.col_ix + a0;
         const uint32_t* __restrict__ Bc = col + T.col_jx;
         const uint32_t* __restrict__ vcol = col + T.col_ij;
@@ -347,33 +365,67 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     h->launches_last = 0;
     h->h2d_last = 0;
 
-    PG_CK(cudaEventRecord(h->ev0, st));
-    // S9: host-resident blocks are copied in for this call.
-    if (h->residency == PGABB_RESIDENT_HOST && h->d_col.n) {
-        PG_CK(cudaMemcpyAsync(h->d_col.p, h->h_col.p, h->d_col.bytes(), cudaMemcpyHostToDevice, st));
-        PG_CK(cudaMemcpyAsync(h->d_rowptr.p, h->h_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyHostToDevice, st));
-        PG_CK(cudaMemcpyAsync(h->d_bitmap.p, h->h_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyHostToDevice, st));
-        h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes() + h->d_bitmap.bytes();
+    const size_t smem = kRowWarps * (kSetWords + 64) * sizeof(uint32_t);
+    static thread_local int cached_dev = -1, grid = 0;
+    if (cached_dev != h->device) {
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int sms = 0, per_sm = 0;
+        PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false>, kRowWarps * 32, smem));
+        grid = sms * std::max(per_sm, 1);
+        cached_dev = h->device;
     }
-    PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
-    PG_CK(cudaEventRecord(h->ev1, st));
-    if (h->n_items) {
-        static thread_local int cached_dev = -1, grid = 0;
-        const size_t smem = kRowWarps * (kSetWords + 64) * sizeof(uint32_t);
-        if (cached_dev != h->device) {
-            PG_CK(cudaFuncSetAttribute(k_tc_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int sms = 0, per_sm = 0;
-            PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-            PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows, kRowWarps * 32, smem));
-            grid = sms * std::max(per_sm, 1);
-            cached_dev = h->device;
+    auto grid_for_items = [&](unsigned long long n) {
+        return (unsigned)std::max(1ull, std::min<unsigned long long>((unsigned long long)grid,
+                                                                     (n + kRowWarps - 1) / kRowWarps));
+    };
+
+    PG_CK(cudaEventRecord(h->ev0, st));
+    if (!h->streaming) {
+        // S9: host-resident blocks are copied in for this call.
+        if (h->residency == PGABB_RESIDENT_HOST && h->d_col.n) {
+            PG_CK(cudaMemcpyAsync(h->d_col.p, h->h_col.p, h->d_col.bytes(), cudaMemcpyHostToDevice, st));
+            PG_CK(cudaMemcpyAsync(h->d_rowptr.p, h->h_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyHostToDevice, st));
+            PG_CK(cudaMemcpyAsync(h->d_bitmap.p, h->h_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyHostToDevice, st));
+            h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes() + h->d_bitmap.bytes();
         }
-        unsigned g = (unsigned)std::min<unsigned long long>((unsigned long long)grid,
-                                                            (h->n_items + kRowWarps - 1) / kRowWarps);
-        k_tc_rows<<<g, kRowWarps * 32, smem, st>>>(h->d_items.p, h->n_items, h->d_tasks.p, h->d_col.p,
-                                                   h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p);
-        PG_LAUNCH_CHECK();
-        h->launches_last++;
+        PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
+        PG_CK(cudaEventRecord(h->ev1, st));
+        if (h->n_items) {
+            k_tc_rows<false><<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
+                h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
+                h->d_task_counts.p);
+            PG_LAUNCH_CHECK();
+            h->launches_last++;
+        }
+    } else {
+        // S9 streaming: wave k's blocks are copied into
+        // arena k%2 on the copy stream while wave k-1 computes; a copy into an arena
+        // first waits for the wave that last used it.
+        PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
+        PG_CK(cudaEventRecord(h->ev1, st));
+        PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev1, 0));
+        const uint32_t* pools[3] = {h->h_col.p, h->h_rowptr.p, h->h_bitmap.p};
+        for (size_t k = 0; k < h->waves.size(); ++k) {
+            const Wave& wv = h->waves[k];
+            const int a = (int)(k & 1);
+            if (k >= 2) PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev_done[a], 0));
+            for (const StagedBlock& c : wv.copies) {
+                PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, pools[c.pool] + c.src_word, c.words * 4,
+                                      cudaMemcpyHostToDevice, h->copy_stream));
+                h->h2d_last += c.words * 4;
+            }
+            PG_CK(cudaEventRecord(h->ev_copied[a], h->copy_stream));
+            PG_CK(cudaStreamWaitEvent(st, h->ev_copied[a], 0));
+            const uint32_t* base = h->d_arena[a].p;
+            k_tc_rows<true><<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
+                nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
+                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p);
+            PG_LAUNCH_CHECK();
+            h->launches_last++;
+            PG_CK(cudaEventRecord(h->ev_done[a], st));
+        }
     }
     PG_CK(cudaEventRecord(h->ev2, st));
     k_sum_tasks<<<1, 1024, 0, st>>>(h->d_task_counts.p, nt, (unsigned long long*)(opts ? opts->d_count : nullptr));

@@ -142,6 +142,27 @@ constexpr uint64_t kDenseInv = 32;
 constexpr uint32_t kWarpBitmapBits = 32768;   // per-warp smem bitmap: 4 KB
 constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
 
+// Streaming residency (S9): host-resident blocks are
+// staged into one of two device arenas per wave of tasks; the copy of wave k+1
+// (copy stream) overlaps the intersections of wave k.
+struct WavePiece {          // one owned piece inside a wave (device table)
+    uint64_t row_prefix;    // first implicit item of the piece within the wave
+    uint32_t task, r0;
+};
+
+struct StagedBlock {        // one H2D copy: pool range -> arena offset (u32 words)
+    uint64_t src_word, dst_word, words;
+    int pool;               // 0 col, 1 rowptr, 2 bitmap
+};
+
+struct Wave {
+    std::vector<StagedBlock> copies;
+    uint64_t words = 0;         // arena words used
+    uint64_t rows = 0;          // implicit items (rows of its pieces)
+    size_t piece_begin = 0, piece_end = 0;   // range in the handle's wave piece table
+    size_t task_table = 0;      // index of this wave's TaskDev table (ntasks entries)
+};
+
 }  // namespace pgabb
 
 struct pgabb_blocks_s {
@@ -177,6 +198,16 @@ struct pgabb_blocks_s {
     uint64_t n_items = 0;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
+
+    // streaming residency (budget > 0 with RESIDENT_HOST)
+    bool streaming = false;
+    uint64_t max_task_bytes = 0;
+    std::vector<pgabb::Wave> waves;
+    pgabb::DBuf<pgabb::WavePiece> d_wave_pieces;
+    pgabb::DBuf<pgabb::TaskDev> d_wave_tasks;         // waves x ntasks, offsets relative to an arena
+    pgabb::DBuf<uint32_t> d_arena[2];
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -194,6 +225,7 @@ namespace pgabb {
 void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint32_t* dst, bool on_device);
 void plan_pieces(pgabb_blocks_s* h);
 void upload_work(pgabb_blocks_s* h);
+void plan_waves(pgabb_blocks_s* h);
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote);
 void resolve_timing(pgabb_blocks_s* h);
 }  // namespace pgabb

@@ -1,0 +1,69 @@
+"""Full-size parity at BASELINE.json's configs, in the launch configuration bench.py
+times (same p, same cut rule, device-resident blocks).
+
+Expected values come from tests/golden/triangles.json, written by
+tests/golden/make_golden.py, which calls only gen/ and oracle/ (never the CUDA
+path); c4 is additionally pinned by its closed form T = 2 * (#diagonal cells).
+c2 is also re-counted by the oracle in the test itself.
+"""
+import json
+import os
+
+import pytest
+
+import gen
+import oracle
+from gen.configs import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2209_04541_b200 as pg  # noqa: E402
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "triangles.json")))
+
+
+def run(name, **kw):
+    cfg = CONFIGS[name]
+    n, s, d = cfg.generate()
+    kw.setdefault("p", cfg.p)
+    with pg.build_blocks(n, s, d, **kw) as b:
+        st = b.stats()
+        T = b.triangle_count()
+    return (n, s, d), T, st
+
+
+def test_c2_vs_oracle_in_job_and_golden():
+    g, T, st = run("c2")
+    assert T == GOLDEN["c2"]["triangles"]
+    assert st["m_edges"] == GOLDEN["c2"]["m_edges"]
+    assert st["wedges"] == GOLDEN["c2"]["wedges"]
+    assert T == oracle.count(*g)
+
+
+@pytest.mark.parametrize("p,rule", [(4, 0), (16, 0), (8, 1), (1, 0)])
+def test_c2_p_invariance(p, rule):
+    _, T, _ = run("c2", p=p, cut_rule=rule)
+    assert T == GOLDEN["c2"]["triangles"]
+
+
+def test_c3_er_full():
+    _, T, st = run("c3")
+    assert T == GOLDEN["c3"]["triangles"]
+    assert st["m_edges"] == GOLDEN["c3"]["m_edges"]
+
+
+def test_c4_grid_full_closed_form():
+    _, T, _ = run("c4")
+    side, f, seed = CONFIGS["c4"].args
+    assert T == 2 * gen.grid_ndiag(side, f, seed) == GOLDEN["c4"]["triangles"]
+
+
+def test_c5_graph500_s26_full():
+    _, T, st = run("c5")
+    assert st["m_edges"] == GOLDEN["c5"]["m_edges"]
+    assert st["wedges"] == GOLDEN["c5"]["wedges"]
+    assert T == GOLDEN["c5"]["triangles"]
