@@ -10,6 +10,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpgabb.so")
+# tooling only (tools/prof_paths.py): an instrumented in-tree build of the same sources
+if os.environ.get("PGABB_LIB_VARIANT") == "prof":
+    LIB_PATH = os.path.join(_HERE, "libpgabb_prof.so")
 
 u32, u64, i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
 u32p = ctypes.POINTER(ctypes.c_uint32)

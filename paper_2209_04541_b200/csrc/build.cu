@@ -506,7 +506,8 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         k_block_offsets<<<grid_for(nb + 1), kThreads, 0, st>>>(bid2.p, mE, nb, d_off.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaMemcpyAsync(off.data(), d_off.p, (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
-        h->d_col.alloc(mE);
+        h->d_col.alloc(mE + kColPad);   // padded: the kernels read 16-byte covers of lists
+        PG_CK(cudaMemsetAsync(h->d_col.p + mE, 0, kColPad * 4, st));
         k_local_cols<<<grid_for(mE), kThreads, 0, st>>>(dag2.p, bid2.p, mE, B, cu, h->d_col.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaStreamSynchronize(st));
@@ -804,7 +805,10 @@ void plan_waves(pgabb_blocks_s* h) {
         PG_CK(cudaMemcpy(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
     uint64_t maxw = 1;
     for (const Wave& wv : h->waves) maxw = std::max(maxw, wv.words);
-    for (int a = 0; a < 2; ++a) h->d_arena[a].alloc(maxw);
+    for (int a = 0; a < 2; ++a) {   // padded like the col pool (16-byte list covers)
+        h->d_arena[a].alloc(maxw + kColPad);
+        PG_CK(cudaMemset(h->d_arena[a].p + maxw, 0, kColPad * 4));
+    }
 }
 
 // This rank's work list: owned pieces in (task, row) order with their pool offsets.

@@ -11,6 +11,21 @@
 
 #include "internal.h"
 
+// PGABB_PROF (tooling build only, tools/prof_paths.py): per-path SM-cycle shares of
+// k_tc_rows, accumulated per warp in registers and flushed once per warp.
+#ifdef PGABB_PROF
+__device__ unsigned long long g_prof[32];
+#define PROF_ARGS , unsigned long long* prof, unsigned long long& pt
+#define PROF_PASS , prof, pt
+#define PROF_MARK(cat) do { const unsigned long long _n = clock64(); prof[cat] += _n - pt; pt = _n; } while (0)
+#define PROF_CNT(cat) (prof[cat] += 1)
+#else
+#define PROF_ARGS
+#define PROF_PASS
+#define PROF_MARK(cat) do { } while (0)
+#define PROF_CNT(cat) do { } while (0)
+#endif
+
 namespace pgabb {
 
 namespace {
@@ -60,7 +75,9 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
 // first) and are dealt cyclically to the warps of the grid (no atomics).
 // ---------------------------------------------------------------------------
 constexpr int kRowWarps = 8;
+constexpr int kRowMinBlocks = 5;   // = the shared-memory limit (5 x 8 warps x 4.4 KB)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
+constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
     return (w * 2654435761u) >> (32 - hbits);
@@ -92,6 +109,22 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
 // a long v list): thread per pair -- the lane binary-searches each element of
 // A_ix[u] (broadcast by shuffle, ascending, so the search window only shrinks)
 // in v's sorted list instead of streaming the whole list.
+// Components c of x with lo <= c < hi (the part of a 16-byte vector inside a list)
+// probed against S.
+template <int MODE>
+__device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int lo, int hi, uint32_t hbits,
+                                           uint32_t hmask) {
+    if (lo <= 0 && hi >= 4)
+        return probe<MODE>(S, x.x, hbits, hmask) + probe<MODE>(S, x.y, hbits, hmask) +
+               probe<MODE>(S, x.z, hbits, hmask) + probe<MODE>(S, x.w, hbits, hmask);
+    uint32_t c = 0;
+    if (lo <= 0 && 0 < hi) c += probe<MODE>(S, x.x, hbits, hmask);
+    if (lo <= 1 && 1 < hi) c += probe<MODE>(S, x.y, hbits, hmask);
+    if (lo <= 2 && 2 < hi) c += probe<MODE>(S, x.z, hbits, hmask);
+    if (lo <= 3 && 3 < hi) c += probe<MODE>(S, x.w, hbits, hmask);
+    return c;
+}
+
 __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
 template <int MODE, int R>
@@ -100,7 +133,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                                                   const uint32_t* __restrict__ Bc,
                                                   const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
                                                   uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
-                                                  const uint32_t* __restrict__ A, uint32_t la, int lane) {
+                                                  const uint32_t* __restrict__ A, uint32_t la, int lane PROF_ARGS) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t le_mask = 0xffffffffu >> (31 - lane);
     uint32_t gsz = 1;
@@ -113,6 +146,8 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
         su[r] = (BM != nullptr && k < W) ? S[k] : 0u;
     }
     uint32_t acc = 0;
+    const uint4* __restrict__ V = reinterpret_cast<const uint4*>((uintptr_t)Bc & ~uintptr_t(15));
+    const uint32_t coff = (uint32_t)(((uintptr_t)Bc & 15) >> 2);   // Bc[0] is word coff of V
     for (uint32_t e = e0; e < e1; e += 32) {
         uint32_t v = 0, b0 = 0, lb = 0;
         if (e + lane < e1) {
@@ -120,6 +155,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             b0 = __ldg(rp_jx + v);
             lb = __ldg(rp_jx + v + 1) - b0;
         }
+        PROF_MARK(9);
         // dense pairs: AND of bitmap rows
         const bool use_and = (BM != nullptr) && lb > W;
         const uint32_t and_mask = __ballot_sync(0xffffffffu, use_and);
@@ -142,6 +178,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 }
             }
             if (use_and) lb = 0;
+            PROF_MARK(3);
         }
         // skewed pairs: binary search of u's elements in v's list
         const bool use_search = lb > 0 && la * log2ceil(lb + 1) * 6u < lb;
@@ -163,49 +200,65 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 }
             }
             if (use_search) lb = 0;
+            PROF_MARK(4);
         }
-        // long lists: one at a time, lanes striding through it (no segment math)
-        uint32_t long_mask = __ballot_sync(0xffffffffu, lb >= 64);
-        while (long_mask) {
-            const int q = __ffs(long_mask) - 1;
-            long_mask &= long_mask - 1;
-            const uint32_t qb0 = __shfl_sync(0xffffffffu, b0, q);
-            const uint32_t qlb = __shfl_sync(0xffffffffu, lb, q);
-            const uint32_t* __restrict__ L = Bc + qb0;
-            uint32_t k = lane;
-            for (; k + 32 < qlb; k += 64) {
-                const uint32_t w0 = __ldg(L + k), w1 = __ldg(L + k + 32);
-                acc += probe<MODE>(S, w0, hbits, hmask) + probe<MODE>(S, w1, hbits, hmask);
-            }
-            if (k < qlb) acc += probe<MODE>(S, __ldg(L + k), hbits, hmask);
-        }
-        if (lb >= 64) lb = 0;
-        // short lists: flattened probing
+        // list pairs: the 16-byte-aligned covers of the batch's remaining lists are
+        // one flattened sequence of uint4 vectors (4 ids each; pools are padded so a
+        // cover never leaves its allocation).  Lane l takes vector positions l, l+32,
+        // ... two rounds at a time (two 16-byte loads in flight per lane); the list of
+        // a position is cur + popc(list starts in (round base, position]), the start
+        // mask from one __reduce_or_sync and cur from one ballot.  Ids outside the
+        // list's [lo, hi) word range (cover head/tail) are masked.
         const uint32_t nonempty = __ballot_sync(0xffffffffu, lb > 0);
         if (nonempty == 0u) continue;
-        uint32_t incl = lb;   // inclusive prefix of list lengths over the batch
+        const uint32_t lo = coff + b0, hi = lo + lb;        // word range in V space
+        const uint32_t nv = lb ? ((hi + 3) >> 2) - (lo >> 2) : 0u;
+        uint32_t incl = nv;   // inclusive prefix of cover lengths over the batch
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t excl = incl - lb;
+        const uint32_t excl = incl - nv;
         __syncwarp();
-        if (lb > 0) scratch[__popc(nonempty & lt_mask)] = b0 - excl;
+        if (lb > 0) {
+            const uint32_t sidx = __popc(nonempty & lt_mask);
+            scratch[sidx] = (lo >> 2) - excl;
+            scratch[32 + sidx] = lo;
+            scratch[64 + sidx] = hi;
+        }
         __syncwarp();
-        for (uint32_t base = 0; base < total; base += 32) {
-            const uint32_t in = excl - base;   // start offset of this lane's list in the round
-            const uint32_t bit = (lb > 0 && excl > base && in < 32u) ? (1u << in) : 0u;
-            const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-            const int cur = __popc(__ballot_sync(0xffffffffu, lb > 0 && excl <= base)) - 1;
-            const uint32_t pos = base + lane;
-            if (pos < total) {
-                const uint32_t seg = cur + __popc(starts & le_mask);
-                const uint32_t w = __ldg(Bc + (pos + scratch[seg]));
-                acc += probe<MODE>(S, w, hbits, hmask);
+        for (uint32_t base = 0; base < total; base += 64) {
+            uint32_t vpos[2], wlo[2], whi[2];
+            uint4 x[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t rb = base + 32 * r;
+                const uint32_t in = excl - rb;
+                const uint32_t bit = (lb > 0 && excl > rb && in < 32u) ? (1u << in) : 0u;
+                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+                const int cur = __popc(__ballot_sync(0xffffffffu, lb > 0 && excl <= rb)) - 1;
+                const uint32_t pos = rb + lane;
+                wlo[r] = 1u;
+                whi[r] = 0u;
+                x[r] = make_uint4(0, 0, 0, 0);
+                vpos[r] = 0;
+                if (pos < total) {
+                    const uint32_t seg = cur + __popc(starts & le_mask);
+                    vpos[r] = pos + scratch[seg];
+                    wlo[r] = scratch[32 + seg];
+                    whi[r] = scratch[64 + seg];
+                    x[r] = __ldg(V + vpos[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int w0 = 4 * (int)vpos[r];
+                acc += probe4<MODE>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask);
             }
         }
+        PROF_MARK(6);
     }
     return acc;
 }
@@ -218,6 +271,29 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ A, uint32_t la,
                                                     const uint32_t* __restrict__ BM, uint32_t W, int lane) {
     uint32_t acc = 0;
+    const uint32_t ne = e1 - e0;
+    if (ne < 32) {
+        // fewer pairs than lanes: flatten (pair q, element k) over the lanes, so
+        // every lane tests a bit; position pos = q * la + k advances by 32 per round
+        const uint32_t vq = (lane < ne) ? __ldg(vcol + e0 + lane) : 0u;
+        uint32_t q = lane / la, k = lane - q * la;
+        const uint32_t dq = 32 / la, dk = 32 - dq * la;
+        const uint32_t P = ne * la;
+        for (uint32_t base = 0; base < P; base += 32) {
+            const uint32_t v = __shfl_sync(0xffffffffu, vq, q & 31);
+            if (base + lane < P) {
+                const uint32_t a = __ldg(A + k);
+                acc += (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
+            }
+            q += dq;
+            k += dk;
+            if (k >= la) {
+                k -= la;
+                ++q;
+            }
+        }
+        return acc;
+    }
     for (uint32_t e = e0; e < e1; e += 32) {
         const bool ok = e + lane < e1;
         const uint32_t v = ok ? __ldg(vcol + e + lane) : 0u;
@@ -239,7 +315,7 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
 // table wp[0..nwp) (rows of empty lists are skipped in the kernel), and the pool
 // pointers all point at the wave's staging arena.
 template <bool IMPLICIT>
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
           unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
@@ -247,13 +323,18 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* S = smem + wid * (kSetWords + 64);
+    uint32_t* S = smem + wid * (kSetWords + kScratchWords);
     uint32_t* scratch = S + kSetWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     __syncwarp();
     const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
     unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid;
     unsigned long long it_next = (!IMPLICIT && idx < nitems) ? __ldg(items + idx) : 0ull;
+#ifdef PGABB_PROF
+    unsigned long long prof[32];
+    for (int c = 0; c < 32; ++c) prof[c] = 0;
+    unsigned long long pt = clock64();
+#endif
     for (; idx < nitems; idx += nwarps) {
         uint32_t t, u;
         if (IMPLICIT) {
@@ -284,22 +365,27 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         while ((1u << hbits) < 2 * la) ++hbits;
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
+        PROF_MARK(0);
         if (T.bm_jx != ~0ull && la <= 2 * T.bm_words) {
             acc = probe_dense_row(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane);
+            PROF_MARK(1);
+            PROF_CNT(16);
         } else if (mode == 0) {
             for (uint32_t k = lane; k < la; k += 32) {
                 const uint32_t w = __ldg(A + k);
                 atomicOr(&S[w >> 5], 1u << (w & 31));
             }
             __syncwarp();
+            PROF_MARK(2);
+            PROF_CNT(17);
             if (T.bm_jx != ~0ull) {
                 const uint32_t* BM = bitmap + T.bm_jx;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = intersect_row<0, 1>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
-                else if (W <= 128) acc = intersect_row<0, 4>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
-                else acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane);
+                if (W <= 32) acc = intersect_row<0, 1>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
+                else if (W <= 128) acc = intersect_row<0, 4>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
+                else acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
             } else {
-                acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane);
+                acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane PROF_PASS);
             }
             __syncwarp();
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
@@ -310,7 +396,9 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
-            acc = intersect_row<1, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane);
+            PROF_MARK(2);
+            PROF_CNT(18);
+            acc = intersect_row<1, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane PROF_PASS);
             __syncwarp();
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
@@ -319,12 +407,20 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 const uint32_t b0 = __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
                 if (b1 > b0) acc += warp_intersect(A, la, Bc + b0, b1 - b0, lane);
             }
+            PROF_MARK(8);
+            PROF_CNT(19);
         }
         __syncwarp();
         // a row's count is < 2^32 (<= |A_ix[u]| * |A_ij[u]|), so a 32-bit REDUX suffices
         const uint32_t sum = __reduce_add_sync(0xffffffffu, acc);
         if (lane == 0 && sum) atomicAdd(&task_counts[t], (unsigned long long)sum);
+        PROF_MARK(7);
     }
+#ifdef PGABB_PROF
+    if (lane == 0)
+        for (int c = 0; c < 32; ++c)
+            if (prof[c]) atomicAdd(&g_prof[c], prof[c]);
+#endif
 }
 
 // S11: T_rank = sum of the per-task counts (written after them, at [ntasks]).
@@ -358,6 +454,19 @@ void resolve_timing(pgabb_blocks_s* h) {
     h->timing_pending = false;
 }
 
+#ifdef PGABB_PROF
+}  // namespace pgabb
+extern "C" PGABB_API int pgabb_prof_read(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, ::g_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return 3;
+    if (reset) {
+        unsigned long long z[32] = {};
+        if (cudaMemcpyToSymbol(::g_prof, z, sizeof(z)) != cudaSuccess) return 3;
+    }
+    return 0;
+}
+namespace pgabb {
+#endif
+
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote) {
     cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
     const bool async = opts && (opts->flags & PGABB_COUNT_ASYNC);
@@ -365,7 +474,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     h->launches_last = 0;
     h->h2d_last = 0;
 
-    const size_t smem = kRowWarps * (kSetWords + 64) * sizeof(uint32_t);
+    const size_t smem = kRowWarps * (kSetWords + kScratchWords) * sizeof(uint32_t);
     static thread_local int cached_dev = -1, grid = 0;
     if (cached_dev != h->device) {
         PG_CK(cudaFuncSetAttribute(k_tc_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -139,6 +139,7 @@ constexpr uint64_t kDenseInv = 32;
 
 // A row item: (task, local row u of part i) with A_ij[u] and A_ix[u] non-empty.
 // Packed as (task << 32) | u; items are sorted by estimated work, heaviest first.
+constexpr uint32_t kColPad = 4;               // u32 words of padding after col pools / arenas
 constexpr uint32_t kWarpBitmapBits = 32768;   // per-warp smem bitmap: 4 KB
 constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
 
