@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
     ap.add_argument("--cut-rule", type=int, default=0)
+    ap.add_argument("--path", choices=["count", "vertex"], default="count",
+                    help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
@@ -260,15 +262,22 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    vertex = args.path == "vertex"
+    tv_dev = torch.zeros(max(n, 1), dtype=torch.int64, device="cuda") if vertex else None
 
     def step():
+        if vertex:
+            # per-vertex t(v) on the device, then one allreduce of the n-vector
+            b.vertex_triangles(stream=stream, out=tv_dev, sync=False)
+            comm.allreduce_(tv_dev)
+            return
         b.triangle_count(stream=stream.cuda_stream, d_count=out.data_ptr(), sync=False)
         comm.allreduce_(out)            # S11: one 8-byte allreduce of the per-rank counts
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    T = int(out.item())
+    T = int(tv_dev.sum().item()) // 3 if vertex else int(out.item())
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kern_ms, launches = [], 0
@@ -296,18 +305,22 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     st = b.stats()
     alg = int(st["alg_bytes_local"])
+    if vertex:
+        # + the t(v) vector: zeroed and read once in rank space, written once in original ids
+        alg += 3 * 8 * n
     kms = statistics.mean(kern_ms) if kern_ms else float("nan")
     achieved = alg / (kms / 1e3) / 1e9 if kms > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.config) if ws == 1 else None,
-                "kernel": "k_tc_rows (S10 intersections)", "kernel_ms": kms,
+                "kernel": "k_tc_rows<VTX> (S10 intersections + t(v) atomics)" if vertex
+                else "k_tc_rows (S10 intersections)", "kernel_ms": kms,
                 "kernel_share_of_step": kms / ms_per_step if ms_per_step else None,
                 "alg_bytes_per_launch": alg, "peak_source": peak_src,
                 "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19"}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not vertex:
         bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
                              residency=pg.RESIDENT_HOST)
         for _ in range(max(1, args.warmup)):
@@ -333,15 +346,16 @@ def run_ours(args):
         bh.free()
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu and not vertex:
         cpu = cpu_baseline(cfg.name, n, s, d, args.cpu_seconds)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC if not vertex else "per-vertex triangle-count edges/sec (|E|/time)",
+            "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n, "tuples": m_tuples, "m_edges": m_edges,
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "path": args.path, "n": n, "tuples": m_tuples, "m_edges": m_edges,
                        "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
                        "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
                        "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}",

@@ -110,6 +110,9 @@ typedef struct {
 } pgabb_count_opts_t;
 
 #define PGABB_COUNT_ASYNC 1u
+#define PGABB_OUT_DEVICE 2u     /* pgabb_vertex_triangles / pgabb_local_clustering: the
+                                   tv and cc arrays are DEVICE pointers on the handle's
+                                   device (stream-ordered on opts->cuda_stream) */
 
 /*
  * S9-S11.  Counts the triangles of the pieces this handle's rank owns (all of
@@ -121,6 +124,36 @@ typedef struct {
  */
 PGABB_API pgabb_status_t pgabb_triangle_count(pgabb_blocks_t b, const pgabb_count_opts_t* opts,
                                     uint64_t* triangles);
+
+/*
+ * Per-vertex triangle counts.  The paper motivates
+ * triangle counting as the way "to measure clustering coefficients"
+ * (§1); t(v) is the number of triangles containing v.
+ * Same S9-S11 path as pgabb_triangle_count; every triangle {u<v<w} (rank
+ * order) found by task (i,j,x) through edge (u,v) in A_ij and w in
+ * A_ix[u] ∩ A_jx[v] adds 1 to t(u), t(v) and t(w).
+ *   tv: uint64[n] indexed by ORIGINAL vertex id; receives this rank's share
+ *       (the sum over ranks is t(v); sum_v t(v) = 3T).  HOST memory, or DEVICE
+ *       memory on the handle's device when opts->flags has PGABB_OUT_DEVICE
+ *       (then the caller may allreduce it over NCCL in place).  Overwritten.
+ *   triangles: optional (NULL allowed); receives this rank's count, as
+ *       pgabb_triangle_count.
+ * PGABB_COUNT_ASYNC is allowed only with PGABB_OUT_DEVICE.
+ * Errors: EINVAL (NULL handle, tv NULL with n > 0), ENOMEM, ECUDA.
+ */
+PGABB_API pgabb_status_t pgabb_vertex_triangles(pgabb_blocks_t b, const pgabb_count_opts_t* opts, uint64_t* tv,
+                                      uint64_t* triangles);
+
+/*
+ * Local clustering coefficient cc(v) = 2 t(v) / (deg(v) (deg(v) - 1)), 0 when
+ * deg(v) < 2 (deg in the canonicalised graph G_s, S1), for every ORIGINAL id v.
+ *   tv: uint64[n], the COMPLETE t(v) (summed over ranks) -- input, borrowed.
+ *   cc: double[n], output.  Both HOST, or both DEVICE with PGABB_OUT_DEVICE.
+ * Computed in fp64 as one correctly rounded division of exact integers.
+ * Synchronous.  Errors: EINVAL (NULL handle / arrays with n > 0), ENOMEM, ECUDA.
+ */
+PGABB_API pgabb_status_t pgabb_local_clustering(pgabb_blocks_t b, const pgabb_count_opts_t* opts,
+                                      const uint64_t* tv, double* cc);
 
 typedef struct {
     uint64_t n, m_tuples, m_edges;      /* m_edges = |E| = |E+| (DESIGN R15) */

@@ -136,6 +136,22 @@ def count(n, src, dst, per_vertex: bool = False):
         return g.count(per_vertex)
 
 
+def clustering(n, src, dst):
+    """Local clustering coefficient of every vertex of G_s (the measure the paper
+    motivates triangle counting with, §1), by its definition:
+    cc(v) = t(v) / C(deg(v), 2) = 2 t(v) / (deg(v) (deg(v) - 1)), and 0 when
+    deg(v) < 2.  t(v) from the node iterator, deg from the oracle's own
+    canonicalisation; one fp64 division of exact integers per vertex.
+    Pinned by tests/test_oracle.py against networkx.clustering and closed forms."""
+    with Graph(n, src, dst) as g:
+        _, tv = g.count(per_vertex=True)
+        deg = g.degrees().astype(np.uint64)
+    cc = np.zeros(int(n), np.float64)
+    m = deg >= 2
+    cc[m] = (2.0 * tv[m].astype(np.float64)) / (deg[m] * (deg[m] - np.uint64(1))).astype(np.float64)
+    return tv, cc
+
+
 def brute(n, src, dst) -> int:
     """O(n^3) brute force over a dense adjacency (n <= 4096)."""
     s, sp = _u32(src)

@@ -105,6 +105,51 @@ class Blocks:
             return None
         return (int(out.value), tc[:self.ntasks]) if task_counts else int(out.value)
 
+    # --- per-vertex counts ---
+    def vertex_triangles(self, stream=None, out=None, sync: bool = True):
+        """This rank's t(v) for every original id v (numpy uint64[n]), or, with
+        ``out`` a CUDA int64/uint64 tensor of n entries, written into it on the
+        device (stream-ordered; ready for an NCCL allreduce).  Returns (tv, T_rank)."""
+        o = _abi.CountOpts()
+        if stream is not None:
+            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+        cnt = ctypes.c_uint64(0)
+        if out is not None:
+            if not getattr(out, "is_cuda", False) or out.numel() < self.n or out.element_size() != 8:
+                raise ValueError("out must be a CUDA 8-byte tensor with >= n entries")
+            o.flags = _abi.OUT_DEVICE | (0 if sync else _abi.COUNT_ASYNC)
+            _ck(_lib.pgabb_vertex_triangles(self._h, ctypes.byref(o), out.data_ptr(), ctypes.byref(cnt)),
+                "pgabb_vertex_triangles")
+            return out, (int(cnt.value) if sync else None)
+        tv = np.zeros(max(self.n, 1), np.uint64)
+        _ck(_lib.pgabb_vertex_triangles(self._h, ctypes.byref(o), tv.ctypes.data, ctypes.byref(cnt)),
+            "pgabb_vertex_triangles")
+        return tv[:self.n], int(cnt.value)
+
+    def local_clustering(self, tv, stream=None):
+        """cc(v) = 2 t(v) / (deg(v)(deg(v)-1)) from the COMPLETE t(v): numpy in ->
+        numpy float64 out, or a CUDA 8-byte tensor in -> CUDA float64 tensor out."""
+        o = _abi.CountOpts()
+        if stream is not None:
+            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+        if getattr(tv, "is_cuda", False):
+            import torch
+            if tv.numel() < self.n or tv.element_size() != 8:
+                raise ValueError("tv must hold n 8-byte counts")
+            tv = tv.contiguous()
+            cc = torch.empty(max(self.n, 1), dtype=torch.float64, device=tv.device)
+            o.flags = _abi.OUT_DEVICE
+            _ck(_lib.pgabb_local_clustering(self._h, ctypes.byref(o), tv.data_ptr(), cc.data_ptr()),
+                "pgabb_local_clustering")
+            return cc[:self.n]
+        t = np.ascontiguousarray(tv, dtype=np.uint64)
+        if t.size < self.n:
+            raise ValueError("tv must hold n counts")
+        cc = np.zeros(max(self.n, 1), np.float64)
+        _ck(_lib.pgabb_local_clustering(self._h, ctypes.byref(o), t.ctypes.data, cc.ctypes.data),
+            "pgabb_local_clustering")
+        return cc[:self.n]
+
     # --- introspection ---
     def stats(self) -> dict:
         s = _abi.Stats()

@@ -23,6 +23,7 @@ vp = ctypes.c_void_p
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ERANGE", 5: "EBUDGET"}
 RESIDENT_DEVICE, RESIDENT_HOST = 0, 1
 COUNT_ASYNC = 1
+OUT_DEVICE = 2
 
 
 class BuildOpts(ctypes.Structure):
@@ -53,6 +54,8 @@ SIGNATURES = [
     ("pgabb_default_build_opts", None, [ctypes.POINTER(BuildOpts)]),
     ("pgabb_build_blocks", ctypes.c_int, [u32, u64, vp, vp, ctypes.POINTER(BuildOpts), ctypes.POINTER(vp)]),
     ("pgabb_triangle_count", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), u64p]),
+    ("pgabb_vertex_triangles", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, u64p]),
+    ("pgabb_local_clustering", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, vp]),
     ("pgabb_get_stats", ctypes.c_int, [vp, ctypes.POINTER(Stats)]),
     ("pgabb_get_rank", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_cuts", ctypes.c_int, [vp, u32p]),

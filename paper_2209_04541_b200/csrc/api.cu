@@ -184,6 +184,42 @@ pgabb_status_t pgabb_triangle_count(pgabb_blocks_t b, const pgabb_count_opts_t* 
     });
 }
 
+pgabb_status_t pgabb_vertex_triangles(pgabb_blocks_t b, const pgabb_count_opts_t* opts, uint64_t* tv,
+                                      uint64_t* triangles) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "handle is NULL");
+        if (!tv && b->n) fail(PGABB_EINVAL, "tv is NULL");
+        if (opts && (opts->flags & PGABB_COUNT_ASYNC) && !(opts->flags & PGABB_OUT_DEVICE))
+            fail(PGABB_EINVAL, "PGABB_COUNT_ASYNC needs PGABB_OUT_DEVICE (a host tv is written synchronously)");
+        DeviceGuard g(b->device);
+        const bool on_dev = opts && (opts->flags & PGABB_OUT_DEVICE);
+        DBuf<unsigned long long> tmp;
+        unsigned long long* d_out = (unsigned long long*)tv;
+        if (!on_dev) {
+            tmp.alloc(std::max<uint32_t>(b->n, 1));
+            d_out = tmp.p;
+        }
+        bool wrote = false;
+        const uint64_t T = count_triangles(b, opts, &wrote, d_out);
+        if (!on_dev && b->n) {
+            cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : b->stream;
+            PG_CK(cudaMemcpyAsync(tv, d_out, (size_t)b->n * 8, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaStreamSynchronize(st));
+        }
+        if (wrote && triangles) *triangles = T;
+    });
+}
+
+pgabb_status_t pgabb_local_clustering(pgabb_blocks_t b, const pgabb_count_opts_t* opts, const uint64_t* tv,
+                                      double* cc) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "handle is NULL");
+        if ((!tv || !cc) && b->n) fail(PGABB_EINVAL, "tv or cc is NULL");
+        DeviceGuard g(b->device);
+        local_clustering(b, opts, tv, cc);
+    });
+}
+
 pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
     return guarded([&] {
         if (!b || !s) fail(PGABB_EINVAL, "NULL argument");

@@ -434,6 +434,10 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         k_scatter_rank<<<grid_for(n), kThreads, 0, st>>>(order.p, n, h->d_rank.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaStreamSynchronize(st));
+        // deg(v) stays with the handle (local clustering coefficient, NEXT-1)
+        h->d_deg.release();
+        std::swap(h->d_deg.p, deg.p);
+        std::swap(h->d_deg.n, deg.n);
     }
 
     // ---- S3 orient + relabel ------------------------------------------------
@@ -791,6 +795,7 @@ void plan_waves(pgabb_blocks_s* h) {
         d.bm_jx = h->blocks[bjx].bm_off == ~0ull ? ~0ull : placed[{bjx, 2}];
         d.bm_words = h->blocks[bjx].bm_words;
         d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
+        d.ci = h->cuts[T.i]; d.cj = h->cuts[T.j]; d.cx = h->cuts[T.x];
         cur_tasks[w.task] = d;
         wpieces.push_back(WavePiece{cur.rows, w.task, w.r0});
         cur.rows += w.r1 - w.r0;
@@ -870,6 +875,7 @@ void upload_work(pgabb_blocks_s* h) {
         d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
         d.bm_jx = bjx.bm_off;
         d.bm_words = bjx.bm_words;
+        d.ci = h->cuts[T.i]; d.cj = h->cuts[T.j]; d.cx = h->cuts[T.x];
         td[t] = d;
     }
     h->d_tasks.alloc(td.size());

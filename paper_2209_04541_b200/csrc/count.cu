@@ -37,8 +37,11 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 
 // Lane-parallel binary search of the shorter list's elements in the longer one.
 // Returns this lane's share of |A ∩ B|.
+// VTX: every common element w also adds 1 to tvx[w] (per-vertex counts, NEXT-1).
+template <bool VTX>
 __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ A, uint32_t la,
-                                                   const uint32_t* __restrict__ B, uint32_t lb, int lane) {
+                                                   const uint32_t* __restrict__ B, uint32_t lb, int lane,
+                                                   unsigned long long* __restrict__ tvx) {
     const uint32_t* S = la <= lb ? A : B;
     const uint32_t* L = la <= lb ? B : A;
     const uint32_t ls = min(la, lb), ll = max(la, lb);
@@ -50,7 +53,9 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
             const uint32_t mid = (lo + hi) >> 1;
             if (__ldg(L + mid) < x) lo = mid + 1; else hi = mid;
         }
-        c += (lo < ll && __ldg(L + lo) == x);
+        const uint32_t hit = (lo < ll && __ldg(L + lo) == x);
+        if (VTX && hit) atomicAdd(tvx + x, 1ull);
+        c += hit;
     }
     return c;
 }
@@ -78,6 +83,8 @@ constexpr int kRowWarps = 8;
 constexpr int kRowMinBlocks = 5;   // = the shared-memory limit (5 x 8 warps x 4.4 KB)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
 constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
+constexpr uint32_t kScratchWordsV = 128;                 // + the batch's v ids (per-vertex kernel)
+__host__ __device__ constexpr uint32_t scratch_words(bool vtx) { return vtx ? kScratchWordsV : kScratchWords; }
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
     return (w * 2654435761u) >> (32 - hbits);
@@ -111,29 +118,43 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
 // in v's sorted list instead of streaming the whole list.
 // Components c of x with lo <= c < hi (the part of a 16-byte vector inside a list)
 // probed against S.
-template <int MODE>
+// VTX: a hit on w also adds 1 to tvx[w] (the triangle's third vertex).
+template <int MODE, bool VTX>
+__device__ __forceinline__ uint32_t probe1(const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask,
+                                           unsigned long long* __restrict__ tvx) {
+    const uint32_t h = probe<MODE>(S, w, hbits, hmask);
+    if (VTX && h) atomicAdd(tvx + w, 1ull);
+    return h;
+}
+
+template <int MODE, bool VTX>
 __device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int lo, int hi, uint32_t hbits,
-                                           uint32_t hmask) {
+                                           uint32_t hmask, unsigned long long* __restrict__ tvx) {
     if (lo <= 0 && hi >= 4)
-        return probe<MODE>(S, x.x, hbits, hmask) + probe<MODE>(S, x.y, hbits, hmask) +
-               probe<MODE>(S, x.z, hbits, hmask) + probe<MODE>(S, x.w, hbits, hmask);
+        return probe1<MODE, VTX>(S, x.x, hbits, hmask, tvx) + probe1<MODE, VTX>(S, x.y, hbits, hmask, tvx) +
+               probe1<MODE, VTX>(S, x.z, hbits, hmask, tvx) + probe1<MODE, VTX>(S, x.w, hbits, hmask, tvx);
     uint32_t c = 0;
-    if (lo <= 0 && 0 < hi) c += probe<MODE>(S, x.x, hbits, hmask);
-    if (lo <= 1 && 1 < hi) c += probe<MODE>(S, x.y, hbits, hmask);
-    if (lo <= 2 && 2 < hi) c += probe<MODE>(S, x.z, hbits, hmask);
-    if (lo <= 3 && 3 < hi) c += probe<MODE>(S, x.w, hbits, hmask);
+    if (lo <= 0 && 0 < hi) c += probe1<MODE, VTX>(S, x.x, hbits, hmask, tvx);
+    if (lo <= 1 && 1 < hi) c += probe1<MODE, VTX>(S, x.y, hbits, hmask, tvx);
+    if (lo <= 2 && 2 < hi) c += probe1<MODE, VTX>(S, x.z, hbits, hmask, tvx);
+    if (lo <= 3 && 3 < hi) c += probe1<MODE, VTX>(S, x.w, hbits, hmask, tvx);
     return c;
 }
 
 __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
-template <int MODE, int R>
+// VTX (per-vertex counts, NEXT-1): each pair's count c_uv is also added to
+// tvj[v], and each common element w adds 1 to tvx[w]; the row total goes to u
+// in the caller.  VTX = false compiles to exactly the counting kernel.
+template <int MODE, int R, bool VTX>
 __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                   const uint32_t* __restrict__ rp_jx,
                                                   const uint32_t* __restrict__ Bc,
                                                   const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
                                                   uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
-                                                  const uint32_t* __restrict__ A, uint32_t la, int lane PROF_ARGS) {
+                                                  const uint32_t* __restrict__ A, uint32_t la, int lane,
+                                                  unsigned long long* __restrict__ tvj,
+                                                  unsigned long long* __restrict__ tvx PROF_ARGS) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t le_mask = 0xffffffffu >> (31 - lane);
     uint32_t gsz = 1;
@@ -167,14 +188,29 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             for (uint32_t q = 0; q < na; q += G) {
                 const uint32_t qq = q + g;
                 if (qq < na) {
-                    const uint32_t* __restrict__ row = BM + (uint64_t)scratch[32 + qq] * W + kl;
+                    const uint32_t vq = scratch[32 + qq];
+                    const uint32_t* __restrict__ row = BM + (uint64_t)vq * W + kl;
+                    uint32_t cv = 0;
                     if (R > 0) {
 #pragma unroll
                         for (int r = 0; r < R; ++r)
-                            if (kl + r * 32 < W) acc += __popc(su[r] & __ldg(row + r * 32));
+                            if (kl + r * 32 < W) {
+                                uint32_t wd = su[r] & __ldg(row + r * 32);
+                                cv += __popc(wd);
+                                if (VTX)
+                                    for (; wd; wd &= wd - 1u)
+                                        atomicAdd(tvx + 32u * (kl + r * 32) + (__ffs(wd) - 1), 1ull);
+                            }
                     } else {
-                        for (uint32_t k = kl; k < W; k += gsz) acc += __popc(S[k] & __ldg(row + (k - kl)));
+                        for (uint32_t k = kl; k < W; k += gsz) {
+                            uint32_t wd = S[k] & __ldg(row + (k - kl));
+                            cv += __popc(wd);
+                            if (VTX)
+                                for (; wd; wd &= wd - 1u) atomicAdd(tvx + 32u * k + (__ffs(wd) - 1), 1ull);
+                        }
                     }
+                    acc += cv;
+                    if (VTX && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
                 }
             }
             if (use_and) lb = 0;
@@ -183,7 +219,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
         // skewed pairs: binary search of u's elements in v's list
         const bool use_search = lb > 0 && la * log2ceil(lb + 1) * 6u < lb;
         if (__any_sync(0xffffffffu, use_search)) {
-            uint32_t lo = 0;
+            uint32_t lo = 0, cv = 0;
             for (uint32_t c = 0; c < la; c += 32) {
                 const uint32_t a = (c + lane < la) ? __ldg(A + c + lane) : 0u;
                 const uint32_t m = min(32u, la - c);
@@ -195,10 +231,14 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                             const uint32_t mid = (lo + hi) >> 1;
                             if (__ldg(Bc + b0 + mid) < ak) lo = mid + 1; else hi = mid;
                         }
-                        acc += (lo < lb && __ldg(Bc + b0 + lo) == ak);
+                        const uint32_t hit = (lo < lb && __ldg(Bc + b0 + lo) == ak);
+                        if (VTX && hit) atomicAdd(tvx + ak, 1ull);
+                        cv += hit;
                     }
                 }
             }
+            acc += cv;
+            if (VTX && cv) atomicAdd(tvj + v, (unsigned long long)cv);
             if (use_search) lb = 0;
             PROF_MARK(4);
         }
@@ -227,10 +267,11 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             scratch[sidx] = (lo >> 2) - excl;
             scratch[32 + sidx] = lo;
             scratch[64 + sidx] = hi;
+            if (VTX) scratch[96 + sidx] = v;
         }
         __syncwarp();
         for (uint32_t base = 0; base < total; base += 64) {
-            uint32_t vpos[2], wlo[2], whi[2];
+            uint32_t vpos[2], wlo[2], whi[2], vv[2];
             uint4 x[2];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
@@ -244,18 +285,22 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 whi[r] = 0u;
                 x[r] = make_uint4(0, 0, 0, 0);
                 vpos[r] = 0;
+                vv[r] = 0;
                 if (pos < total) {
                     const uint32_t seg = cur + __popc(starts & le_mask);
                     vpos[r] = pos + scratch[seg];
                     wlo[r] = scratch[32 + seg];
                     whi[r] = scratch[64 + seg];
+                    if (VTX) vv[r] = scratch[96 + seg];
                     x[r] = __ldg(V + vpos[r]);
                 }
             }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int w0 = 4 * (int)vpos[r];
-                acc += probe4<MODE>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask);
+                const uint32_t c = probe4<MODE, VTX>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, tvx);
+                acc += c;
+                if (VTX && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
             }
         }
         PROF_MARK(6);
@@ -267,9 +312,12 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
 // takes v_l and tests each element a of A_ix[u] (broadcast by shuffle) against
 // bit a of v_l's bitmap row.  Costs |A_ix[u]| bit tests per pair instead of W
 // word ANDs, and needs no staging of u at all.
+template <bool VTX>
 __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                     const uint32_t* __restrict__ A, uint32_t la,
-                                                    const uint32_t* __restrict__ BM, uint32_t W, int lane) {
+                                                    const uint32_t* __restrict__ BM, uint32_t W, int lane,
+                                                    unsigned long long* __restrict__ tvj,
+                                                    unsigned long long* __restrict__ tvx) {
     uint32_t acc = 0;
     const uint32_t ne = e1 - e0;
     if (ne < 32) {
@@ -283,7 +331,12 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
             const uint32_t v = __shfl_sync(0xffffffffu, vq, q & 31);
             if (base + lane < P) {
                 const uint32_t a = __ldg(A + k);
-                acc += (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
+                const uint32_t hit = (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
+                if (VTX && hit) {
+                    atomicAdd(tvx + a, 1ull);
+                    atomicAdd(tvj + v, 1ull);
+                }
+                acc += hit;
             }
             q += dq;
             k += dk;
@@ -298,14 +351,21 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
         const bool ok = e + lane < e1;
         const uint32_t v = ok ? __ldg(vcol + e + lane) : 0u;
         const uint32_t* __restrict__ row = BM + (uint64_t)v * W;
+        uint32_t cv = 0;
         for (uint32_t c = 0; c < la; c += 32) {
             const uint32_t a = (c + lane < la) ? __ldg(A + c + lane) : 0u;
             const uint32_t m = min(32u, la - c);
             for (uint32_t k = 0; k < m; ++k) {
                 const uint32_t ak = __shfl_sync(0xffffffffu, a, k);
-                if (ok) acc += (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u;
+                if (ok) {
+                    const uint32_t hit = (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u;
+                    if (VTX && hit) atomicAdd(tvx + ak, 1ull);
+                    cv += hit;
+                }
             }
         }
+        acc += cv;
+        if (VTX && cv) atomicAdd(tvj + v, (unsigned long long)cv);
     }
     return acc;
 }
@@ -314,16 +374,19 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
 // IMPLICIT = true (streaming residency): item idx is row idx of the wave's piece
 // table wp[0..nwp) (rows of empty lists are skipped in the kernel), and the pool
 // pointers all point at the wave's staging arena.
-template <bool IMPLICIT>
+// VTX = true (per-vertex counts, NEXT-1): tv[rank-space id] += the triangles
+// found here that contain the vertex -- u gets the row total, v each pair's
+// c_uv, w one per hit -- so sum over ranks of tv = t(v) and sum tv = 3T.
+template <bool IMPLICIT, bool VTX>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
           unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
-          unsigned long long* __restrict__ task_counts) {
+          unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* S = smem + wid * (kSetWords + kScratchWords);
+    uint32_t* S = smem + wid * (kSetWords + scratch_words(VTX));
     uint32_t* scratch = S + kSetWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     __syncwarp();
@@ -365,9 +428,11 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         while ((1u << hbits) < 2 * la) ++hbits;
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
+        unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
+        unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
         PROF_MARK(0);
         if (T.bm_jx != ~0ull && la <= 2 * T.bm_words) {
-            acc = probe_dense_row(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane);
+            acc = probe_dense_row<VTX>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);
         } else if (mode == 0) {
@@ -381,11 +446,11 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             if (T.bm_jx != ~0ull) {
                 const uint32_t* BM = bitmap + T.bm_jx;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = intersect_row<0, 1>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
-                else if (W <= 128) acc = intersect_row<0, 4>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
-                else acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane PROF_PASS);
+                if (W <= 32) acc = intersect_row<0, 1, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
+                else if (W <= 128) acc = intersect_row<0, 4, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
+                else acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
             } else {
-                acc = intersect_row<0, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane PROF_PASS);
+                acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
             }
             __syncwarp();
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
@@ -398,14 +463,18 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             __syncwarp();
             PROF_MARK(2);
             PROF_CNT(18);
-            acc = intersect_row<1, 0>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane PROF_PASS);
+            acc = intersect_row<1, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, tvx PROF_PASS);
             __syncwarp();
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
             for (uint32_t e = e0; e < e1; ++e) {
                 const uint32_t v = __ldg(vcol + e);
                 const uint32_t b0 = __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
-                if (b1 > b0) acc += warp_intersect(A, la, Bc + b0, b1 - b0, lane);
+                if (b1 > b0) {
+                    const uint32_t c = warp_intersect<VTX>(A, la, Bc + b0, b1 - b0, lane, tvx);
+                    if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+                    acc += c;
+                }
             }
             PROF_MARK(8);
             PROF_CNT(19);
@@ -413,7 +482,10 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         __syncwarp();
         // a row's count is < 2^32 (<= |A_ix[u]| * |A_ij[u]|), so a 32-bit REDUX suffices
         const uint32_t sum = __reduce_add_sync(0xffffffffu, acc);
-        if (lane == 0 && sum) atomicAdd(&task_counts[t], (unsigned long long)sum);
+        if (lane == 0 && sum) {
+            atomicAdd(&task_counts[t], (unsigned long long)sum);
+            if (VTX) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
+        }
         PROF_MARK(7);
     }
 #ifdef PGABB_PROF
@@ -438,6 +510,24 @@ __global__ void k_sum_tasks(unsigned long long* tc, int nt, unsigned long long* 
             tc[nt] = s;
             if (out_dev) *out_dev = s;
         }
+    }
+}
+
+// Per-vertex counts back to original ids: tv[v] = tv_rank[rank[v]].
+__global__ void k_gather_tv(const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ tv_rank,
+                            uint32_t n, unsigned long long* __restrict__ tv) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        tv[v] = tv_rank[rank[v]];
+}
+
+// Local clustering coefficient (NEXT-1): cc(v) = 2 t(v) / (deg(v) (deg(v) - 1)),
+// 0 for deg(v) < 2.  Both operands are exact in fp64 (< 2^53), so the one IEEE
+// division is correctly rounded and bit-identical to any other such evaluation.
+__global__ void k_clustering(const uint32_t* __restrict__ deg, const unsigned long long* __restrict__ tv,
+                             uint32_t n, double* __restrict__ cc) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint64_t d = deg[v];
+        cc[v] = d < 2 ? 0.0 : (2.0 * (double)tv[v]) / (double)(d * (d - 1));
     }
 }
 
@@ -467,27 +557,45 @@ extern "C" PGABB_API int pgabb_prof_read(unsigned long long* out, int reset) {
 namespace pgabb {
 #endif
 
-uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote) {
+uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
+                         unsigned long long* d_tv_out) {
     cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
     const bool async = opts && (opts->flags & PGABB_COUNT_ASYNC);
     const int nt = (int)h->tasks.size();
     h->launches_last = 0;
     h->h2d_last = 0;
 
-    const size_t smem = kRowWarps * (kSetWords + kScratchWords) * sizeof(uint32_t);
-    static thread_local int cached_dev = -1, grid = 0;
+    const bool vtx = d_tv_out != nullptr;
+    const size_t smem = kRowWarps * (kSetWords + scratch_words(vtx)) * sizeof(uint32_t);
+    static thread_local int cached_dev = -1, grid_c = 0, grid_v = 0;
     if (cached_dev != h->device) {
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const size_t sm_c = kRowWarps * (kSetWords + scratch_words(false)) * sizeof(uint32_t);
+        const size_t sm_v = kRowWarps * (kSetWords + scratch_words(true)) * sizeof(uint32_t);
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
         int sms = 0, per_sm = 0;
         PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false>, kRowWarps * 32, smem));
-        grid = sms * std::max(per_sm, 1);
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, false>, kRowWarps * 32, sm_c));
+        grid_c = sms * std::max(per_sm, 1);
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, true>, kRowWarps * 32, sm_v));
+        grid_v = sms * std::max(per_sm, 1);
         cached_dev = h->device;
     }
+    const int grid = vtx ? grid_v : grid_c;
     auto grid_for_items = [&](unsigned long long n) {
         return (unsigned)std::max(1ull, std::min<unsigned long long>((unsigned long long)grid,
                                                                      (n + kRowWarps - 1) / kRowWarps));
+    };
+    unsigned long long* tv = nullptr;
+    if (vtx) {
+        if (h->d_tv_rank.n < std::max<uint32_t>(h->n, 1)) h->d_tv_rank.alloc(std::max<uint32_t>(h->n, 1));
+        tv = h->d_tv_rank.p;
+    }
+    auto rows_kernel = [&](bool implicit) {
+        if (implicit) return vtx ? k_tc_rows<true, true> : k_tc_rows<true, false>;
+        return vtx ? k_tc_rows<false, true> : k_tc_rows<false, false>;
     };
 
     PG_CK(cudaEventRecord(h->ev0, st));
@@ -500,11 +608,12 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes() + h->d_bitmap.bytes();
         }
         PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
+        if (vtx) PG_CK(cudaMemsetAsync(tv, 0, (size_t)h->n * sizeof(unsigned long long), st));
         PG_CK(cudaEventRecord(h->ev1, st));
         if (h->n_items) {
-            k_tc_rows<false><<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
+            rows_kernel(false)<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
                 h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p);
+                h->d_task_counts.p, tv);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -513,6 +622,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         // arena k%2 on the copy stream while wave k-1 computes; a copy into an arena
         // first waits for the wave that last used it.
         PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
+        if (vtx) PG_CK(cudaMemsetAsync(tv, 0, (size_t)h->n * sizeof(unsigned long long), st));
         PG_CK(cudaEventRecord(h->ev1, st));
         PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev1, 0));
         const uint32_t* pools[3] = {h->h_col.p, h->h_rowptr.p, h->h_bitmap.p};
@@ -528,9 +638,9 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             PG_CK(cudaEventRecord(h->ev_copied[a], h->copy_stream));
             PG_CK(cudaStreamWaitEvent(st, h->ev_copied[a], 0));
             const uint32_t* base = h->d_arena[a].p;
-            k_tc_rows<true><<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
+            rows_kernel(true)<<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
                 nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p);
+                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv);
             PG_LAUNCH_CHECK();
             h->launches_last++;
             PG_CK(cudaEventRecord(h->ev_done[a], st));
@@ -540,6 +650,12 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     k_sum_tasks<<<1, 1024, 0, st>>>(h->d_task_counts.p, nt, (unsigned long long*)(opts ? opts->d_count : nullptr));
     PG_LAUNCH_CHECK();
     h->launches_last++;
+    if (vtx && h->n) {
+        k_gather_tv<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, 148 * 16), 256, 0, st>>>(
+            h->d_rank.p, tv, h->n, d_tv_out);
+        PG_LAUNCH_CHECK();
+        h->launches_last++;
+    }
     PG_CK(cudaMemcpyAsync(h->h_result.p, h->d_task_counts.p + nt, 8, cudaMemcpyDeviceToHost, st));
     PG_CK(cudaEventRecord(h->ev3, st));
     h->timing_pending = true;
@@ -555,6 +671,28 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     }
     *wrote = true;
     return h->h_result.p[0];
+}
+
+void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc) {
+    cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
+    const bool on_dev = opts && (opts->flags & PGABB_OUT_DEVICE);
+    if (h->n == 0) return;
+    DBuf<unsigned long long> d_tv;
+    DBuf<double> d_cc;
+    const unsigned long long* tvp = (const unsigned long long*)tv;
+    double* ccp = cc;
+    if (!on_dev) {
+        d_tv.alloc(h->n);
+        d_cc.alloc(h->n);
+        PG_CK(cudaMemcpyAsync(d_tv.p, tv, (size_t)h->n * 8, cudaMemcpyHostToDevice, st));
+        tvp = d_tv.p;
+        ccp = d_cc.p;
+    }
+    k_clustering<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, 148 * 16), 256, 0, st>>>(h->d_deg.p, tvp,
+                                                                                         h->n, ccp);
+    PG_LAUNCH_CHECK();
+    if (!on_dev) PG_CK(cudaMemcpyAsync(cc, d_cc.p, (size_t)h->n * 8, cudaMemcpyDeviceToHost, st));
+    PG_CK(cudaStreamSynchronize(st));
 }
 
 }  // namespace pgabb

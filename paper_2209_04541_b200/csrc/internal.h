@@ -130,6 +130,8 @@ struct TaskDev {
     uint64_t bm_jx;          // bitmap-pool offset of dense A_jx rows, ~0 if A_jx is list-only
     uint32_t wx;             // width of column part x (bits of a bitmap over it)
     uint32_t bm_words;       // words per dense row of A_jx
+    uint32_t ci, cj, cx;     // rank-space first vertex of parts i, j, x (cuts; per-vertex counts)
+    uint32_t pad;
 };
 
 // A block gets a dense bitmap copy (rows of ceil(w/32) words) when its density is
@@ -185,6 +187,8 @@ struct pgabb_blocks_s {
     std::vector<uint32_t> task_of_ijx;          // p^3 -> task id or kNoTask
 
     pgabb::DBuf<uint32_t> d_rank;               // original id -> rank
+    pgabb::DBuf<uint32_t> d_deg;                // original id -> degree in G_s (S2; clustering)
+    pgabb::DBuf<unsigned long long> d_tv_rank;  // per-vertex counts, rank space (allocated on demand)
     pgabb::DBuf<uint32_t> d_col;                // col pool (local col ids), block-major
     pgabb::DBuf<uint32_t> d_rowptr;             // rowptr pool (block-local edge offsets)
     pgabb::DBuf<uint32_t> d_bitmap;             // dense-block bitmap pool (rows of bm_words)
@@ -227,6 +231,8 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
 void plan_pieces(pgabb_blocks_s* h);
 void upload_work(pgabb_blocks_s* h);
 void plan_waves(pgabb_blocks_s* h);
-uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote);
+uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
+                         unsigned long long* d_tv_out = nullptr);
+void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc);
 void resolve_timing(pgabb_blocks_s* h);
 }  // namespace pgabb

@@ -42,3 +42,28 @@ def combine_counts_host(local: int, group=None) -> int:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return int(t.item())
+
+
+def vertex_triangles_allreduce(b: Blocks, out=None, group=None):
+    """t(v) for every original id: this rank's share written on the device, then
+    ONE NCCL allreduce(sum) of the n-entry int64 vector (the exchange step of the
+    per-vertex path; t(v) < 2^63).  Returns the device tensor."""
+    import torch
+    import torch.distributed as dist
+    if out is None:
+        out = torch.empty(max(b.n, 1), dtype=torch.int64, device="cuda")
+    b.vertex_triangles(stream=torch.cuda.current_stream(), out=out, sync=False)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out[:b.n]
+
+
+def combine_vertex_counts_host(local, group=None):
+    """Allreduce of host-side per-vertex partials (CPU/gloo path used by the tests)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(local, dtype=np.int64))
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t.numpy().astype(np.uint64)

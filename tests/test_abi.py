@@ -75,5 +75,7 @@ def test_null_arguments_rejected():
     assert lib.pgabb_build_blocks(3, 0, None, None, None, None) == 1   # out NULL -> EINVAL
     assert b"NULL" in lib.pgabb_last_error()
     assert lib.pgabb_triangle_count(None, None, None) == 1
+    assert lib.pgabb_vertex_triangles(None, None, None, None) == 1
+    assert lib.pgabb_local_clustering(None, None, None, None) == 1
     lib.pgabb_free(None)   # no-op
     assert pg.version().startswith("pgabb")

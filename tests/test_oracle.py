@@ -206,3 +206,30 @@ def test_bad_ids_rejected():
 def test_empty_graph():
     assert oracle.count(0, np.zeros(0, np.uint32), np.zeros(0, np.uint32)) == 0
     assert oracle.count(5, np.zeros(0, np.uint32), np.zeros(0, np.uint32)) == 0
+
+
+# ---- local clustering coefficient (NEXT-1) -------------------
+def test_clustering_vs_networkx():
+    for n, s, d in (gen.rmat(9, 8, seed=5), gen.er_small(200, 0.08, seed=6), gen.king(7, 9)):
+        G = nx.Graph()
+        G.add_nodes_from(range(n))
+        G.add_edges_from((int(a), int(b)) for a, b in zip(s, d) if a != b)
+        _, cc = oracle.clustering(n, s, d)
+        ref = nx.clustering(G)
+        # both are one correctly rounded division of the same integers
+        assert [float(x) for x in cc] == [float(ref[v]) for v in range(n)]
+
+
+def test_clustering_closed_forms():
+    _, cc = oracle.clustering(*gen.complete(12))
+    assert (cc == 1.0).all()                          # every neighbourhood of K_n is a clique
+    n = 40
+    tv, cc = oracle.clustering(*gen.wheel(n))         # hub 0 + (n-1)-cycle
+    assert tv[0] == n - 1 and (tv[1:] == 2).all()
+    assert cc[0] == 2.0 * (n - 1) / ((n - 1) * (n - 2)) and (cc[1:] == 2.0 * 2 / (3 * 2)).all()
+    for g in (gen.random_tree(300, 2), gen.cycle(50), gen.complete_bipartite(5, 8)):
+        _, cc = oracle.clustering(*g)
+        assert (cc == 0.0).all()
+    e = np.zeros(0, np.uint32)
+    tv, cc = oracle.clustering(5, e, e)               # isolated vertices: deg < 2 -> 0
+    assert (tv == 0).all() and (cc == 0.0).all()

@@ -16,6 +16,9 @@ def summarize(path):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
         name = r["Kernel Name"].split("(")[0].replace("pgabb::<unnamed>::", "")
+        if name.startswith("void "):
+            name = name[5:]
+        name = name.split("<")[0] if name.startswith("k_") else name   # k_tc_rows<0, 0> -> k_tc_rows
         unit = r["Metric Unit"]
         v = float(r["Metric Value"].replace(",", ""))
         ns = v * {"ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "s": 1e9}.get(unit, 1)
