@@ -76,6 +76,9 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_bitmap.release();
     d_tasks.release();
     d_items.release();
+    d_light.release();
+    d_deg.release();
+    d_tv_rank.release();
     h_result.release();
     for (cudaEvent_t e : {ev0, ev1, ev2, ev3})
         if (e) cudaEventDestroy(e);

@@ -298,17 +298,38 @@ __global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsig
 }
 
 // Row items of one owned piece: rows u in [r0, r1) with A_ij[u] and A_ix[u]
-// non-empty.  flags[r - r0] = 1 for those rows (flags[nrows] = 0 for the scan).
-__global__ void k_row_flags(PieceDev w, const uint32_t* rowptr, uint32_t* flags) {
+// non-empty, classified by their work (DESIGN R20): LIGHT rows -- |A_ix[u]| <=
+// kLightLa, |A_ij[u]| <= kLightLe and at most kLightWork list loads for the
+// thread-per-row kernel (a v list of <= kLightScan ids is scanned, a longer one
+// is binary-searched per element of A_ix[u]; a dense A_jx costs one bit test per
+// element) -- get lf = 1; every other row gets hf = 1 (warp per row).
+// hf[nrows] = lf[nrows] = 0 for the exclusive scans.
+__global__ void k_row_flags(PieceDev w, const uint32_t* col, const uint32_t* rowptr, int dense_jx, uint32_t* hf,
+                            uint32_t* lf) {
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= nr;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t f = 0;
+        uint32_t fh = 0, fl = 0;
         if (k < nr) {
             const uint32_t u = w.r0 + (uint32_t)k;
-            f = (rowptr[w.rp_ij + u + 1] > rowptr[w.rp_ij + u]) && (rowptr[w.rp_ix + u + 1] > rowptr[w.rp_ix + u]);
+            const uint32_t e0 = rowptr[w.rp_ij + u], e1 = rowptr[w.rp_ij + u + 1];
+            const uint32_t la = rowptr[w.rp_ix + u + 1] - rowptr[w.rp_ix + u];
+            if (e1 > e0 && la > 0) {
+                bool light = la <= kLightLa && e1 - e0 <= kLightLe;
+                if (light && !dense_jx) {
+                    uint32_t work = 0;
+                    for (uint32_t e = e0; e < e1 && work <= kLightWork; ++e) {
+                        const uint32_t v = col[w.col_ij + e];
+                        work += light_pair_loads(la, rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v]);
+                    }
+                    light = work <= kLightWork;
+                }
+                fl = light;
+                fh = !light;
+            }
         }
-        flags[k] = f;
+        hf[k] = fh;
+        lf[k] = fl;
     }
 }
 
@@ -354,6 +375,8 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         h->cuts = {0, n};
         h->blocks.assign(1, BlockInfo{});
         h->blocks[0].nrows = n;
+        h->d_deg.alloc(std::max<uint32_t>(n, 1));
+        PG_CK(cudaMemsetAsync(h->d_deg.p, 0, (size_t)std::max<uint32_t>(n, 1) * 4, st));
         if (n) {
             k_iota<<<grid_for(n), kThreads, 0, st>>>(h->d_rank.p, n);
             PG_LAUNCH_CHECK();
@@ -908,43 +931,64 @@ void upload_work(pgabb_blocks_s* h) {
     const std::vector<size_t> order = locality_order(h);
     uint32_t maxrows = 0;
     for (const PieceDev& w : h->work) maxrows = std::max(maxrows, w.r1 - w.r0);
-    DBuf<uint32_t> flags, pos;
+    DBuf<uint32_t> hf, lf, hpos, lpos;
     DBuf<unsigned char> tmp;
-    flags.alloc((size_t)maxrows + 1);
-    pos.alloc((size_t)maxrows + 1);
-    std::vector<uint64_t> piece_items(h->work.size(), 0);
+    hf.alloc((size_t)maxrows + 1);
+    lf.alloc((size_t)maxrows + 1);
+    hpos.alloc((size_t)maxrows + 1);
+    lpos.alloc((size_t)maxrows + 1);
+    std::vector<uint64_t> piece_items(h->work.size(), 0), piece_light(h->work.size(), 0);
+    auto classify = [&](const PieceDev& w) {
+        const uint32_t nr = w.r1 - w.r0;
+        const Task& T = h->tasks[w.task];
+        const int dense = h->blocks[T.j * h->p + T.x].bm_off != ~0ull;
+        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, dense, hf.p, lf.p);
+        PG_LAUNCH_CHECK();
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(tp, b, hf.p, hpos.p, (int64_t)nr + 1, st);
+        }, st, tmp);
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(tp, b, lf.p, lpos.p, (int64_t)nr + 1, st);
+        }, st, tmp);
+    };
     // pass 1: count per piece
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
-        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_rowptr.p, flags.p);
-        PG_LAUNCH_CHECK();
-        cub_call([&](void* tp, size_t& b) {
-            return cub::DeviceScan::ExclusiveSum(tp, b, flags.p, pos.p, (int64_t)nr + 1, st);
-        }, st, tmp);
-        uint32_t cntp = 0;
-        PG_CK(cudaMemcpyAsync(&cntp, pos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+        classify(w);
+        uint32_t cnt[2] = {0, 0};
+        PG_CK(cudaMemcpyAsync(&cnt[0], hpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaMemcpyAsync(&cnt[1], lpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
         PG_CK(cudaStreamSynchronize(st));
-        piece_items[k] = cntp;
+        piece_items[k] = cnt[0];
+        piece_light[k] = cnt[1];
     }
-    uint64_t nitems = 0;
-    for (uint64_t c : piece_items) nitems += c;
+    uint64_t nitems = 0, nlight = 0;
+    for (size_t k = 0; k < piece_items.size(); ++k) {
+        nitems += piece_items[k];
+        nlight += piece_light[k];
+    }
     h->n_items = nitems;
+    h->n_light = nlight;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
+    h->d_light.alloc(std::max<uint64_t>(nlight, 1));
     // pass 2: emit in layout order
-    uint64_t base = 0;
+    uint64_t base = 0, lbase = 0;
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
-        if (!piece_items[k]) continue;
-        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_rowptr.p, flags.p);
-        PG_LAUNCH_CHECK();
-        cub_call([&](void* tp, size_t& b) {
-            return cub::DeviceScan::ExclusiveSum(tp, b, flags.p, pos.p, (int64_t)nr + 1, st);
-        }, st, tmp);
-        k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, flags.p, pos.p, h->d_items.p + base);
-        PG_LAUNCH_CHECK();
+        if (!piece_items[k] && !piece_light[k]) continue;
+        classify(w);
+        if (piece_items[k]) {
+            k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, hf.p, hpos.p, h->d_items.p + base);
+            PG_LAUNCH_CHECK();
+        }
+        if (piece_light[k]) {
+            k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, lf.p, lpos.p, h->d_light.p + lbase);
+            PG_LAUNCH_CHECK();
+        }
         base += piece_items[k];
+        lbase += piece_light[k];
     }
     PG_CK(cudaStreamSynchronize(st));
 }

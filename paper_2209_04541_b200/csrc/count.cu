@@ -495,6 +495,112 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// k_tc_light: one THREAD per light row item (DESIGN R20) -- the low-degree rows
+// that dominate sparse graphs (ER, road-like grids), where a warp per row would
+// spend its time on latency with one or two list elements per lane.
+//
+//   A_ix[u] (<= kLightLa ids) is held in registers (unused slots = ~0u, never a
+//   local id);
+//   for each v in A_ij[u] (<= kLightLe):
+//     dense A_jx:  one bit test of v's bitmap row per element of A_ix[u];
+//     |A_jx[v]| <= kLightScan: every id of the list compared with all of A_ix[u];
+//     longer:      binary search of each element of A_ix[u] in the list.
+// Items are dealt cyclically over the grid (coalesced item loads); a thread keeps
+// its count while consecutive items share a task and flushes it with one
+// atomicAdd when the task changes.  Same exact |A_ix[u] ∩ A_jx[v]| sums as
+// k_tc_rows (Listing 5).
+// ---------------------------------------------------------------------------
+constexpr int kLightThreads = 256;
+
+template <bool VTX>
+__global__ void __launch_bounds__(kLightThreads)
+k_tc_light(const unsigned long long* __restrict__ items, unsigned long long nitems,
+           const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
+           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
+           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    uint32_t cur_t = 0xffffffffu;
+    unsigned long long acc_t = 0;
+    for (unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; idx < nitems;
+         idx += stride) {
+        const unsigned long long it = __ldg(items + idx);
+        const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
+        if (t != cur_t) {
+            if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+            cur_t = t;
+            acc_t = 0;
+        }
+        const TaskDev& T = tasks[t];
+        const uint64_t rp_ix = T.rp_ix, rp_ij = T.rp_ij, col_ij = T.col_ij, bm_jx = T.bm_jx;
+        const uint32_t a0 = __ldg(rowptr + rp_ix + u), a1 = __ldg(rowptr + rp_ix + u + 1);
+        const uint32_t e0 = __ldg(rowptr + rp_ij + u), e1 = __ldg(rowptr + rp_ij + u + 1);
+        const uint32_t la = a1 - a0;
+        const uint32_t* __restrict__ A = col + T.col_ix + a0;
+        uint32_t a[kLightLa];
+#pragma unroll
+        for (int k = 0; k < (int)kLightLa; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
+        unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
+        unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
+        uint32_t acc = 0;
+        if (bm_jx != ~0ull) {
+            const uint32_t W = T.bm_words;
+            const uint32_t* __restrict__ BM = bitmap + bm_jx;
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t v = __ldg(col + col_ij + e);
+                const uint32_t* __restrict__ row = BM + (uint64_t)v * W;
+                uint32_t c = 0;
+#pragma unroll
+                for (int k = 0; k < (int)kLightLa; ++k)
+                    if (k < (int)la) {
+                        const uint32_t hit = (__ldg(row + (a[k] >> 5)) >> (a[k] & 31)) & 1u;
+                        if (VTX && hit) atomicAdd(tvx + a[k], 1ull);
+                        c += hit;
+                    }
+                acc += c;
+                if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+            }
+        } else {
+            const uint64_t rp_jx = T.rp_jx;
+            const uint32_t* __restrict__ Bc = col + T.col_jx;
+            for (uint32_t e = e0; e < e1; ++e) {
+                const uint32_t v = __ldg(col + col_ij + e);
+                const uint32_t b0 = __ldg(rowptr + rp_jx + v), b1 = __ldg(rowptr + rp_jx + v + 1);
+                const uint32_t lb = b1 - b0;
+                uint32_t c = 0;
+                if (lb <= kLightScan) {
+                    for (uint32_t q = b0; q < b1; ++q) {
+                        const uint32_t x = __ldg(Bc + q);
+                        uint32_t hit = 0;
+#pragma unroll
+                        for (int k = 0; k < (int)kLightLa; ++k) hit |= (x == a[k]);
+                        if (VTX && hit) atomicAdd(tvx + x, 1ull);
+                        c += hit;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < (int)kLightLa; ++k)
+                        if (k < (int)la) {
+                            uint32_t lo = b0, hi = b1;
+                            while (lo < hi) {
+                                const uint32_t mid = (lo + hi) >> 1;
+                                if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
+                            }
+                            const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
+                            if (VTX && hit) atomicAdd(tvx + a[k], 1ull);
+                            c += hit;
+                        }
+                }
+                acc += c;
+                if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+            }
+        }
+        acc_t += acc;
+        if (VTX && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
+    }
+    if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+}
+
 // S11: T_rank = sum of the per-task counts (written after them, at [ntasks]).
 __global__ void k_sum_tasks(unsigned long long* tc, int nt, unsigned long long* out_dev) {
     unsigned long long s = 0;
@@ -613,6 +719,23 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         if (h->n_items) {
             rows_kernel(false)<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
                 h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
+                h->d_task_counts.p, tv);
+            PG_LAUNCH_CHECK();
+            h->launches_last++;
+        }
+        if (h->n_light) {
+            static thread_local int light_dev = -1, light_grid = 0;
+            if (light_dev != h->device) {
+                int sms = 0, per_sm = 0;
+                PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false>, kLightThreads, 0));
+                light_grid = sms * std::max(per_sm, 1);
+                light_dev = h->device;
+            }
+            const unsigned g = (unsigned)std::max<unsigned long long>(
+                1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
+            (vtx ? k_tc_light<true> : k_tc_light<false>)<<<g, kLightThreads, 0, st>>>(
+                h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
                 h->d_task_counts.p, tv);
             PG_LAUNCH_CHECK();
             h->launches_last++;

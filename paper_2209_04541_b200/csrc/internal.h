@@ -145,6 +145,20 @@ constexpr uint32_t kColPad = 4;               // u32 words of padding after col 
 constexpr uint32_t kWarpBitmapBits = 32768;   // per-warp smem bitmap: 4 KB
 constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
 
+// Light rows (DESIGN R20): handled one per thread by k_tc_light, A_ix[u] held in
+// registers.  A v list of <= kLightScan ids is scanned (each id compared with all
+// of A_ix[u]); a longer one is binary-searched once per element of A_ix[u].
+constexpr uint32_t kLightLa = 8;       // |A_ix[u]| <= 8 (the register copy)
+constexpr uint32_t kLightLe = 32;      // |A_ij[u]| <= 32 pairs
+constexpr uint32_t kLightScan = 16;
+constexpr uint32_t kLightWork = 128;   // list loads per row
+__host__ __device__ inline uint32_t light_pair_loads(uint32_t la, uint32_t lb) {
+    if (lb <= kLightScan) return lb;
+    uint32_t lg = 0;
+    while ((1u << lg) < lb + 1) ++lg;
+    return la * lg;
+}
+
 // Streaming residency (S9): host-resident blocks are
 // staged into one of two device arenas per wave of tasks; the copy of wave k+1
 // (copy stream) overlaps the intersections of wave k.
@@ -199,8 +213,10 @@ struct pgabb_blocks_s {
     uint64_t work_edges = 0;
     pgabb::DBuf<pgabb::PieceDev> d_work;
     pgabb::DBuf<pgabb::TaskDev> d_tasks;             // ntasks descriptors
-    pgabb::DBuf<unsigned long long> d_items;         // row items, heaviest first
+    pgabb::DBuf<unsigned long long> d_items;         // heavy row items (warp per row)
     uint64_t n_items = 0;
+    pgabb::DBuf<unsigned long long> d_light;         // light row items (thread per row, DESIGN R20)
+    uint64_t n_light = 0;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
 
