@@ -64,13 +64,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(config):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+def load_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` on `config` from the committed
+    ncu --set full summary (profiles/ncu_summary.json, written by tools/make_profile.py)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             js = json.load(f)
-        return js.get(config, {}).get("dram_bytes_per_launch")
+        return js.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -280,7 +281,7 @@ def run_ours(args):
     T = int(tv_dev.sum().item()) // 3 if vertex else int(out.item())
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern_ms, launches = [], 0
+    kern_ms, light_ms, launches = [], [], 0
     with ClockSampler(dev) as clk:
         comm.barrier()
         torch.cuda.synchronize()
@@ -292,6 +293,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             stk = b.stats()
             kern_ms.append(stk["ms_main_kernel_last"])
+            light_ms.append(stk["ms_light_kernel_last"])
             launches += int(stk["launches_last"])
         torch.cuda.synchronize()
         comm.barrier()
@@ -309,14 +311,24 @@ def run_ours(args):
         # + the t(v) vector: zeroed and read once in rank space, written once in original ids
         alg += 3 * 8 * n
     kms = statistics.mean(kern_ms) if kern_ms else float("nan")
-    achieved = alg / (kms / 1e3) / 1e9 if kms > 0 else 0.0
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.config) if ws == 1 else None,
-                "kernel": "k_tc_rows<VTX> (S10 intersections + t(v) atomics)" if vertex
-                else "k_tc_rows (S10 intersections)", "kernel_ms": kms,
-                "kernel_share_of_step": kms / ms_per_step if ms_per_step else None,
-                "alg_bytes_per_launch": alg, "peak_source": peak_src,
-                "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19"}
+    lms = statistics.mean(light_ms) if light_ms else 0.0
+    alg_l = int(st["alg_bytes_light"])
+
+    def kern(name, ms, nbytes):
+        ach = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        return {"kernel": name, "ms": ms, "alg_bytes": nbytes, "achieved": ach, "frac": ach / peak}
+    # S10 runs as two kernels (DESIGN R20): warp-per-row k_tc_rows, thread-per-row k_tc_light
+    kernels = [kern("k_tc_rows", kms - lms, alg - alg_l), kern("k_tc_light", lms, alg_l)]
+    dom = max(kernels, key=lambda k: k["ms"])
+    both = kern("k_tc_rows + k_tc_light", kms, alg)
+    roofline = {"bound": "hbm", "achieved": dom["achieved"], "peak": peak, "unit": "GB/s",
+                "frac": dom["frac"], "traffic": load_traffic(args.config, dom["kernel"]) if ws == 1 else None,
+                "kernel": dom["kernel"] + ("<VTX> (S10 + t(v) atomics)" if vertex else " (S10 intersections)"),
+                "kernel_ms": dom["ms"], "kernel_share_of_step": dom["ms"] / ms_per_step if ms_per_step else None,
+                "alg_bytes_per_launch": dom["alg_bytes"], "peak_source": peak_src,
+                "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19",
+                "kernels": kernels, "s10_combined": both,
+                "items": {"heavy": int(st["items_heavy"]), "light": int(st["items_light"])}}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None

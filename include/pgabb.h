@@ -166,11 +166,14 @@ typedef struct {
     uint64_t launches_last;             /* kernels launched by the last count call */
     uint64_t waves;                     /* streaming residency: waves per count (0 otherwise) */
     uint64_t max_task_bytes;            /* largest block-triple footprint (col+rowptr+dense copy) */
-    uint64_t reserved[2];
+    uint64_t items_heavy, items_light;  /* this rank's row items: warp per row / thread per row (DESIGN R20) */
+    uint64_t alg_bytes_light;           /* staged-model bytes of the light items (within alg_bytes_local) */
+    uint64_t reserved[1];
     double ms_build;                    /* wall time of pgabb_build_blocks */
     double ms_count_last;               /* device time of the last count call (events) */
-    double ms_main_kernel_last;         /* device time of the intersection kernels */
-    double reserved_d[3];
+    double ms_main_kernel_last;         /* device time of the intersection kernels (heavy + light) */
+    double ms_light_kernel_last;        /* device time of the light-row kernel alone */
+    double reserved_d[2];
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);

@@ -167,19 +167,22 @@ def task_cost(B, t) -> int:
 
 
 def task_alg_bytes(B, t) -> int:
-    """Staged model (reading R19): 4*(sum over rows u with edges of
-    |A_ix[u]| + sum over edges (u,v) of |A_jx[v]|) + 12*nnz(A_ij)."""
+    """Staged model (reading R19): over the rows u of part i with
+    A_ij[u] and A_ix[u] both non-empty (a row with an empty A_ix[u] has nothing to
+    intersect), 4*(|A_ix[u]| + sum over v in A_ij[u] of |A_jx[v]|) + 12*|A_ij[u]|."""
     i, j, x = t
     rp_ij, col = B[(i, j)]
     rp_ix = B[(i, x)][0]
     rp_jx = B[(j, x)][0]
-    el = 0
+    total = 0
     for r in range(rp_ij.size - 1):
-        if rp_ij[r + 1] > rp_ij[r]:
-            el += rp_ix[r + 1] - rp_ix[r]
-    for v in col:
-        el += rp_jx[v + 1] - rp_jx[v]
-    return int(4 * el + 12 * col.size)
+        la = int(rp_ix[r + 1] - rp_ix[r])
+        vs = col[rp_ij[r]:rp_ij[r + 1]]
+        if la == 0 or vs.size == 0:
+            continue
+        el = la + sum(int(rp_jx[v + 1] - rp_jx[v]) for v in vs)
+        total += 4 * el + 12 * vs.size
+    return int(total)
 
 
 # S8 -- pieces and LPT (PAPER.md:756-757, 843-849 §4.1/§4.4 "sorts them in

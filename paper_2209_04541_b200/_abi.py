@@ -42,8 +42,10 @@ class Stats(ctypes.Structure):
                 ("npieces", u64), ("npieces_local", u64), ("wedges", u64), ("cost_total", u64),
                 ("cost_local", u64), ("alg_bytes_total", u64), ("alg_bytes_local", u64),
                 ("block_bytes", u64), ("h2d_bytes_last", u64), ("launches_last", u64),
-                ("waves", u64), ("max_task_bytes", u64), ("reserved", u64 * 2), ("ms_build", ctypes.c_double), ("ms_count_last", ctypes.c_double),
-                ("ms_main_kernel_last", ctypes.c_double), ("reserved_d", ctypes.c_double * 3)]
+                ("waves", u64), ("max_task_bytes", u64), ("items_heavy", u64), ("items_light", u64),
+                ("alg_bytes_light", u64), ("reserved", u64 * 1), ("ms_build", ctypes.c_double),
+                ("ms_count_last", ctypes.c_double), ("ms_main_kernel_last", ctypes.c_double),
+                ("ms_light_kernel_last", ctypes.c_double), ("reserved_d", ctypes.c_double * 2)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}

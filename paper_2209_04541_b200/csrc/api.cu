@@ -80,7 +80,7 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_deg.release();
     d_tv_rank.release();
     h_result.release();
-    for (cudaEvent_t e : {ev0, ev1, ev2, ev3})
+    for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_mid})
         if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (prev >= 0) cudaSetDevice(prev);
@@ -128,7 +128,7 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h = new pgabb_blocks_s();
         h->device = dev;
         PG_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev0, &h->ev1, &h->ev2, &h->ev3}) PG_CK(cudaEventCreate(e));
+        for (cudaEvent_t* e : {&h->ev0, &h->ev1, &h->ev2, &h->ev3, &h->ev_mid}) PG_CK(cudaEventCreate(e));
         h->h_result.alloc(1);
         h->n = n;
         h->m_tuples = m;
@@ -251,6 +251,10 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->ms_build = b->ms_build;
         s->ms_count_last = b->ms_count_last;
         s->ms_main_kernel_last = b->ms_main_last;
+        s->ms_light_kernel_last = b->ms_light_last;
+        s->items_heavy = b->n_items;
+        s->items_light = b->n_light;
+        s->alg_bytes_light = b->alg_light;
     });
 }
 

@@ -223,7 +223,7 @@ struct CostArg {
     CutsArg cu;
     unsigned long long mE;
     unsigned long long* cost;
-    unsigned long long* alg_el;
+    unsigned long long* alg_bytes;
 };
 
 // Launched per non-empty block (i, j): every lane of a warp shares the block, so
@@ -247,19 +247,21 @@ __global__ void k_task_costs(CostArg a, int i, int j) {
         for (int x = j; x < a.p; ++x) {
             const uint32_t t = a.tid[(i * a.p + j) * a.p + x];
             if (t == kNoTask) continue;
-            uint32_t c = 0, el = 0;
+            uint32_t c = 0;
+            unsigned long long by = 0;
             if (ok) {
                 const BlockDev bix = a.blk[i * a.p + x], bjx = a.blk[j * a.p + x];
                 const uint32_t la = a.rowptr[bix.rp_off + u + 1] - a.rowptr[bix.rp_off + u];
                 const uint32_t lb = a.rowptr[bjx.rp_off + v + 1] - a.rowptr[bjx.rp_off + v];
                 c = la + lb;
-                el = lb + (first ? la : 0u);
+                // staged model (DESIGN R19): only rows with A_ix[u] non-empty move bytes
+                if (la) by = 4ull * (lb + (first ? la : 0u)) + 12ull;
             }
             c = __reduce_add_sync(0xffffffffu, c);
-            el = __reduce_add_sync(0xffffffffu, el);
+            for (int o = 16; o > 0; o >>= 1) by += __shfl_down_sync(0xffffffffu, by, o);
             if (lane == 0) {
                 atomicAdd(&a.cost[t], (unsigned long long)c);
-                atomicAdd(&a.alg_el[t], (unsigned long long)el);
+                atomicAdd(&a.alg_bytes[t], by);
             }
         }
     }
@@ -304,32 +306,45 @@ __global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsig
 // is binary-searched per element of A_ix[u]; a dense A_jx costs one bit test per
 // element) -- get lf = 1; every other row gets hf = 1 (warp per row).
 // hf[nrows] = lf[nrows] = 0 for the exclusive scans.
+// alg (nullable): += staged-model bytes of the light rows (DESIGN R19), for the
+// per-kernel roofline.
 __global__ void k_row_flags(PieceDev w, const uint32_t* col, const uint32_t* rowptr, int dense_jx, uint32_t* hf,
-                            uint32_t* lf) {
+                            uint32_t* lf, unsigned long long* alg) {
     const uint32_t nr = w.r1 - w.r0;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= nr;
-         k += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t k0 = blockIdx.x * (uint64_t)blockDim.x; k0 <= nr; k0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = k0 + threadIdx.x;
         uint32_t fh = 0, fl = 0;
+        unsigned long long bytes = 0;
         if (k < nr) {
             const uint32_t u = w.r0 + (uint32_t)k;
             const uint32_t e0 = rowptr[w.rp_ij + u], e1 = rowptr[w.rp_ij + u + 1];
             const uint32_t la = rowptr[w.rp_ix + u + 1] - rowptr[w.rp_ix + u];
             if (e1 > e0 && la > 0) {
                 bool light = la <= kLightLa && e1 - e0 <= kLightLe;
-                if (light && !dense_jx) {
-                    uint32_t work = 0;
-                    for (uint32_t e = e0; e < e1 && work <= kLightWork; ++e) {
+                if (light) {
+                    uint32_t work = 0, lsum = 0;
+                    for (uint32_t e = e0; e < e1; ++e) {
                         const uint32_t v = col[w.col_ij + e];
-                        work += light_pair_loads(la, rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v]);
+                        const uint32_t lb = rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v];
+                        work += light_pair_loads(la, lb);
+                        lsum += lb;
                     }
-                    light = work <= kLightWork;
+                    light = dense_jx || work <= kLightWork;
+                    bytes = 4ull * (la + lsum) + 12ull * (e1 - e0);
                 }
                 fl = light;
                 fh = !light;
+                if (!light) bytes = 0;
             }
         }
-        hf[k] = fh;
-        lf[k] = fl;
+        if (k <= nr) {
+            hf[k] = fh;
+            lf[k] = fl;
+        }
+        if (alg) {
+            for (int o = 16; o > 0; o >>= 1) bytes += __shfl_down_sync(0xffffffffu, bytes, o);
+            if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(alg, bytes);
+        }
     }
 }
 
@@ -634,7 +649,7 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_CK(cudaMemsetAsync(d_alg.p, 0, nt * 8, st));
         CostArg a;
         a.dag = dag; a.col = h->d_col.p; a.rowptr = h->d_rowptr.p; a.blk = d_blk.p; a.tid = d_tid.p;
-        a.B = B; a.p = (int)p; a.cu = cu; a.mE = mE; a.cost = d_cost.p; a.alg_el = d_alg.p;
+        a.B = B; a.p = (int)p; a.cu = cu; a.mE = mE; a.cost = d_cost.p; a.alg_bytes = d_alg.p;
         for (uint32_t i = 0; i < p; ++i)
             for (uint32_t j = i; j < p; ++j) {
                 const BlockInfo& b = h->blocks[i * p + j];
@@ -651,8 +666,7 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         for (size_t t = 0; t < nt; ++t) {
             Task& T = h->tasks[t];
             T.cost = c[t];
-            T.alg_el = ae[t];
-            T.alg_bytes = 4 * ae[t] + 12 * h->blocks[T.i * p + T.j].nnz;
+            T.alg_bytes = ae[t];
             h->cost_total += T.cost;
             h->alg_total += T.alg_bytes;
         }
@@ -938,11 +952,14 @@ void upload_work(pgabb_blocks_s* h) {
     hpos.alloc((size_t)maxrows + 1);
     lpos.alloc((size_t)maxrows + 1);
     std::vector<uint64_t> piece_items(h->work.size(), 0), piece_light(h->work.size(), 0);
-    auto classify = [&](const PieceDev& w) {
+    DBuf<unsigned long long> d_alg;
+    d_alg.alloc(1);
+    PG_CK(cudaMemsetAsync(d_alg.p, 0, 8, st));
+    auto classify = [&](const PieceDev& w, unsigned long long* alg) {
         const uint32_t nr = w.r1 - w.r0;
         const Task& T = h->tasks[w.task];
         const int dense = h->blocks[T.j * h->p + T.x].bm_off != ~0ull;
-        k_row_flags<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, dense, hf.p, lf.p);
+        k_row_flags<<<grid_for(nr + 1), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, dense, hf.p, lf.p, alg);
         PG_LAUNCH_CHECK();
         cub_call([&](void* tp, size_t& b) {
             return cub::DeviceScan::ExclusiveSum(tp, b, hf.p, hpos.p, (int64_t)nr + 1, st);
@@ -955,7 +972,7 @@ void upload_work(pgabb_blocks_s* h) {
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
-        classify(w);
+        classify(w, d_alg.p);
         uint32_t cnt[2] = {0, 0};
         PG_CK(cudaMemcpyAsync(&cnt[0], hpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
         PG_CK(cudaMemcpyAsync(&cnt[1], lpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
@@ -970,6 +987,9 @@ void upload_work(pgabb_blocks_s* h) {
     }
     h->n_items = nitems;
     h->n_light = nlight;
+    unsigned long long alg_light = 0;
+    PG_CK(cudaMemcpy(&alg_light, d_alg.p, 8, cudaMemcpyDeviceToHost));
+    h->alg_light = alg_light;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
     h->d_light.alloc(std::max<uint64_t>(nlight, 1));
     // pass 2: emit in layout order
@@ -978,7 +998,7 @@ void upload_work(pgabb_blocks_s* h) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
         if (!piece_items[k] && !piece_light[k]) continue;
-        classify(w);
+        classify(w, nullptr);
         if (piece_items[k]) {
             k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, hf.p, hpos.p, h->d_items.p + base);
             PG_LAUNCH_CHECK();

@@ -80,6 +80,17 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
 // first) and are dealt cyclically to the warps of the grid (no atomics).
 // ---------------------------------------------------------------------------
 constexpr int kRowWarps = 8;
+constexpr int kRowChunk = 4;       // row items per warp claim
+
+// Claims the next kRowChunk items for the calling warp; returns the first (>= n: done).
+__device__ __forceinline__ unsigned long long claim_items(unsigned long long* next, unsigned long long n, int lane,
+                                                          unsigned long long& end) {
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(next, (unsigned long long)kRowChunk);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    end = b + kRowChunk < n ? b + kRowChunk : n;
+    return b;
+}
 constexpr int kRowMinBlocks = 5;   // = the shared-memory limit (5 x 8 warps x 4.4 KB)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
 constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
@@ -382,7 +393,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
           unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
-          unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv) {
+          unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
+          unsigned long long* __restrict__ next) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -391,14 +403,18 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     __syncwarp();
     const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
-    unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid;
-    unsigned long long it_next = (!IMPLICIT && idx < nitems) ? __ldg(items + idx) : 0ull;
+    // IMPLICIT: items dealt cyclically.  Otherwise warps claim kRowChunk items at a
+    // time from one counter, so the items in flight stay a narrow window of the
+    // locality-ordered list (the A_jx blocks they share stay in L2).
+    unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid, claim_end = 0;
+    if (!IMPLICIT) idx = claim_items(next, nitems, lane, claim_end);
 #ifdef PGABB_PROF
     unsigned long long prof[32];
     for (int c = 0; c < 32; ++c) prof[c] = 0;
     unsigned long long pt = clock64();
 #endif
-    for (; idx < nitems; idx += nwarps) {
+    for (; idx < nitems; idx = IMPLICIT ? idx + nwarps : (idx + 1 < claim_end ? idx + 1
+                                                                             : claim_items(next, nitems, lane, claim_end))) {
         uint32_t t, u;
         if (IMPLICIT) {
             int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
@@ -409,8 +425,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             t = wp[lo].task;
             u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
         } else {
-            const unsigned long long it = it_next;
-            if (idx + nwarps < nitems) it_next = __ldg(items + idx + nwarps);   // prefetch the next item
+            const unsigned long long it = __ldg(items + idx);
             t = (uint32_t)(it >> 32);
             u = (uint32_t)it;
         }
@@ -506,24 +521,35 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 //     dense A_jx:  one bit test of v's bitmap row per element of A_ix[u];
 //     |A_jx[v]| <= kLightScan: every id of the list compared with all of A_ix[u];
 //     longer:      binary search of each element of A_ix[u] in the list.
-// Items are dealt cyclically over the grid (coalesced item loads); a thread keeps
-// its count while consecutive items share a task and flushes it with one
-// atomicAdd when the task changes.  Same exact |A_ix[u] ∩ A_jx[v]| sums as
+// Items are claimed in order by warps, kLightChunk x 32 at a time from one global
+// counter (lane l takes items base + 32r + l: coalesced item loads), so the
+// items in flight stay a narrow window of the locality-ordered list and the
+// v-side block A_jx they probe stays in L2.  A thread keeps its count while
+// consecutive items share a task and flushes it with one atomicAdd when the
+// task changes.  Same exact |A_ix[u] ∩ A_jx[v]| sums as
 // k_tc_rows (Listing 5).
 // ---------------------------------------------------------------------------
 constexpr int kLightThreads = 256;
+constexpr int kLightChunk = 8;   // items per lane per claim
 
 template <bool VTX>
 __global__ void __launch_bounds__(kLightThreads)
 k_tc_light(const unsigned long long* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
-           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
+           unsigned long long* __restrict__ next) {
+    const int lane = threadIdx.x & 31;
     uint32_t cur_t = 0xffffffffu;
     unsigned long long acc_t = 0;
-    for (unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; idx < nitems;
-         idx += stride) {
+    for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(next, (unsigned long long)(32 * kLightChunk));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= nitems) break;
+    for (int r = 0; r < kLightChunk; ++r) {
+        const unsigned long long idx = base + 32 * r + lane;
+        if (idx >= nitems) break;
         const unsigned long long it = __ldg(items + idx);
         const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
         if (t != cur_t) {
@@ -598,6 +624,7 @@ k_tc_light(const unsigned long long* __restrict__ items, unsigned long long nite
         acc_t += acc;
         if (VTX && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
     }
+    }
     if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
 }
 
@@ -645,6 +672,9 @@ void resolve_timing(pgabb_blocks_s* h) {
     float ms = 0, ms_main = 0;
     PG_CK(cudaEventElapsedTime(&ms, h->ev0, h->ev3));
     PG_CK(cudaEventElapsedTime(&ms_main, h->ev1, h->ev2));
+    float ms_light = 0;
+    if (h->light_timed) PG_CK(cudaEventElapsedTime(&ms_light, h->ev_mid, h->ev2));
+    h->ms_light_last = ms_light;
     h->ms_count_last = ms;
     h->ms_main_last = ms_main;
     h->timing_pending = false;
@@ -672,6 +702,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     h->h2d_last = 0;
 
     const bool vtx = d_tv_out != nullptr;
+    h->light_timed = false;
     const size_t smem = kRowWarps * (kSetWords + scratch_words(vtx)) * sizeof(uint32_t);
     static thread_local int cached_dev = -1, grid_c = 0, grid_v = 0;
     if (cached_dev != h->device) {
@@ -715,14 +746,17 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
         PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
         if (vtx) PG_CK(cudaMemsetAsync(tv, 0, (size_t)h->n * sizeof(unsigned long long), st));
+        PG_CK(cudaMemsetAsync(h->d_next.p, 0, 2 * sizeof(unsigned long long), st));
         PG_CK(cudaEventRecord(h->ev1, st));
         if (h->n_items) {
             rows_kernel(false)<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
                 h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p, tv);
+                h->d_task_counts.p, tv, h->d_next.p + 1);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
+        PG_CK(cudaEventRecord(h->ev_mid, st));
+        h->light_timed = true;
         if (h->n_light) {
             static thread_local int light_dev = -1, light_grid = 0;
             if (light_dev != h->device) {
@@ -736,7 +770,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
                 1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
             (vtx ? k_tc_light<true> : k_tc_light<false>)<<<g, kLightThreads, 0, st>>>(
                 h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p, tv);
+                h->d_task_counts.p, tv, h->d_next.p);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -763,7 +797,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             const uint32_t* base = h->d_arena[a].p;
             rows_kernel(true)<<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
                 nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv);
+                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
             PG_CK(cudaEventRecord(h->ev_done[a], st));

@@ -99,8 +99,8 @@ struct BlockInfo {
 struct Task {
     uint32_t i, j, x;
     uint64_t cost = 0;       // S7: sum_{(u,v) in A_ij} (|A_ix[u]| + |A_jx[v]|)
-    uint64_t alg_el = 0;     // staged-model elements (DESIGN R19)
-    uint64_t alg_bytes = 0;  // 4*alg_el + 12*nnz(A_ij)
+    uint64_t alg_bytes = 0;  // staged model (DESIGN R19): rows u with A_ij[u], A_ix[u] non-empty,
+                             // 4*(|A_ix[u]| + sum_v |A_jx[v]|) + 12*|A_ij[u]|
 };
 
 struct Piece {
@@ -231,12 +231,14 @@ struct pgabb_blocks_s {
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
 
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev_mid = nullptr;
 
     // stats
     uint64_t cost_total = 0, cost_local = 0, alg_total = 0, alg_local = 0;
     uint64_t h2d_last = 0, launches_last = 0;
-    double ms_build = 0, ms_count_last = 0, ms_main_last = 0;
+    double ms_build = 0, ms_count_last = 0, ms_main_last = 0, ms_light_last = 0;
+    uint64_t alg_light = 0;                   // staged-model bytes of the light items
+    bool light_timed = false;                 // ev_mid recorded by the last count
     bool timing_pending = false;   // events of the last (async) count not read yet
 
     ~pgabb_blocks_s();

@@ -50,7 +50,7 @@ def test_struct_layouts():
     from paper_2209_04541_b200 import _abi
     assert ctypes.sizeof(_abi.BuildOpts) == 40
     assert ctypes.sizeof(_abi.CountOpts) == 32
-    assert ctypes.sizeof(_abi.Stats) == 19 * 8 + 6 * 8   # layout unchanged: waves + max_task_bytes took 2 reserved slots
+    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # 17 counters + items_heavy/light, alg_bytes_light, 1 reserved; 6 doubles
 
 
 def test_sm100a_cubin(lib_path):

@@ -170,6 +170,41 @@ def test_cost_k3_p2_hand():
     assert P.alg_bytes == [36, 16]
 
 
+def test_alg_bytes_skip_rows_without_x_neighbours():
+    # star with centre c and leaves; ranks: leaves first (deg 1), centre last.  Add a
+    # triangle among three leaves to create DAG rows with edges into some parts only.
+    # Pinned against an independent restatement over the DAG (no block CSR):
+    #   sum over tasks (i,j,x), over u in part i with N+_j(u), N+_x(u) both non-empty, of
+    #   4*(|N+_x(u)| + sum_{v in N+_j(u)} |N+_x(v)|) + 12*|N+_j(u)|.
+    for g, p in ((gen.rmat(8, 8, seed=7), 3), (gen.er_small(120, 0.06, seed=8), 4), (gen.king(6, 7), 5)):
+        P = ob.Plan(*g, p=p)
+        part = np.searchsorted(np.asarray(P.cuts), np.arange(g[0]), side="right") - 1
+        nplus = {}
+        for a_, b_ in P.D:
+            nplus.setdefault(int(a_), []).append(int(b_))
+        def nx_(u, x):
+            return [w for w in nplus.get(u, []) if part[w] == x]
+        want = []
+        for (i, j, x) in P.tasks:
+            tot = 0
+            for u in range(g[0]):
+                if part[u] != i:
+                    continue
+                nj, nxu = nx_(u, j), nx_(u, x)
+                if nj and nxu:
+                    tot += 4 * (len(nxu) + sum(len(nx_(v, x)) for v in nj)) + 12 * len(nj)
+            want.append(tot)
+        assert P.alg_bytes == want
+        # rows without x-neighbours really occur here (the old all-rows model differs)
+        old = 0
+        for (i, j, x) in P.tasks:
+            for u in range(g[0]):
+                nj = nx_(u, j) if part[u] == i else []
+                if nj:
+                    old += 4 * (len(nx_(u, x)) + sum(len(nx_(v, x)) for v in nj)) + 12 * len(nj)
+        assert sum(want) < old
+
+
 # ---- S8 pieces and LPT -------------------------------------------------------------
 def test_pieces_k4_hand():
     # G=2: cap = ceil(18/8) = 3, k = 6; row costs [12,5,1,0], R=[0,12,17,18,18]

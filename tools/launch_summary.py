@@ -1,6 +1,6 @@
 """Compact summary of an ncu launch list (--metrics gpu__time_duration.sum --csv):
 per kernel name, launch count and total / mean device time, and each kernel's
-share of the count-phase launches (k_tc_rows + k_sum_tasks)."""
+share of the count-phase launches (k_tc_rows + k_tc_light + k_sum_tasks)."""
 import csv
 import collections
 import json
@@ -28,7 +28,7 @@ def summarize(path):
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += ns
-    count_phase = {k: v for k, v in agg.items() if k in ("k_tc_rows", "k_sum_tasks")}
+    count_phase = {k: v for k, v in agg.items() if k in ("k_tc_rows", "k_tc_light", "k_sum_tasks")}
     tot = sum(v[1] for v in count_phase.values()) or 1.0
     out = {k: {"launches": v[0], "total_ms": v[1] / 1e6, "mean_ms": v[1] / v[0] / 1e6,
                "share_of_count_phase": (v[1] / tot) if k in count_phase else None} for k, v in agg.items()}

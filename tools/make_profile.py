@@ -33,25 +33,30 @@ def main(tag, config, rnd="01"):
     lc = os.path.join(g, f"launches_{tag}.csv")
     if os.path.exists(lc):
         s = summarize(lc)
-        out["launches"] = {k: v for k, v in s.items() if k in ("k_tc_rows", "k_sum_tasks")}
-        out["launches_build_total_ms"] = sum(v["total_ms"] for k, v in s.items()
-                                             if k not in ("k_tc_rows", "k_sum_tasks"))
+        cp = ("k_tc_rows", "k_tc_light", "k_sum_tasks")
+        out["launches"] = {k: v for k, v in s.items() if k in cp}
+        out["launches_build_total_ms"] = sum(v["total_ms"] for k, v in s.items() if k not in cp)
         out["launches_note"] = ("ncu launch list (--metrics gpu__time_duration.sum --clock-control none): "
                                 "cold-cache, serialised; compare shares, not absolutes")
     rep = os.path.join(g, f"prof_{tag}.ncu-rep")
     if os.path.exists(rep):
-        ks = [d for d in summary(rep) if "k_tc_rows" in d["kernel"]]
-        if ks:
+        ns = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        js = json.load(open(ns)) if os.path.exists(ns) else {}
+        entry = js.get(config, {})
+        entry = {k: v for k, v in entry.items() if k.startswith("k_")}   # per-kernel entries only
+        for kname in ("k_tc_rows", "k_tc_light"):
+            ks = [d for d in summary(rep) if kname in d["kernel"]]
+            if not ks:
+                continue
             k = ks[0]
-            out["ncu_k_tc_rows"] = k
+            out[f"ncu_{kname}"] = k
             traffic = to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"])
-            out["dram_bytes_per_launch"] = traffic
-            ns = os.path.join(ROOT, "profiles", "ncu_summary.json")
-            js = json.load(open(ns)) if os.path.exists(ns) else {}
-            js[config] = {"dram_bytes_per_launch": traffic, "source": f"profiles/r{rnd}_{tag}.json",
-                          "l2_hit_pct": k.get("lts__t_sector_hit_rate.pct"),
-                          "kernel_ms_under_ncu": k.get("gpu__time_duration.sum")}
-            json.dump(js, open(ns, "w"), indent=1, sort_keys=True)
+            out[f"dram_bytes_per_launch_{kname}"] = traffic
+            entry[kname] = {"dram_bytes_per_launch": traffic, "source": f"profiles/r{rnd}_{tag}.json",
+                            "l2_hit_pct": k.get("lts__t_sector_hit_rate.pct"),
+                            "kernel_ms_under_ncu": k.get("gpu__time_duration.sum")}
+        js[config] = entry
+        json.dump(js, open(ns, "w"), indent=1, sort_keys=True)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     path = os.path.join(ROOT, "profiles", f"r{rnd}_{tag}.json")
     json.dump(out, open(path, "w"), indent=1)
