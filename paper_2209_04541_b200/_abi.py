@@ -10,9 +10,10 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpgabb.so")
-# tooling only (tools/prof_paths.py): an instrumented in-tree build of the same sources
-if os.environ.get("PGABB_LIB_VARIANT") == "prof":
-    LIB_PATH = os.path.join(_HERE, "libpgabb_prof.so")
+# tooling only (tools/prof_paths.py, tools/variants.py): an in-tree build of the same
+# sources with other compile-time switches (instrumentation, kernel-variant A/B runs)
+if os.environ.get("PGABB_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, "libpgabb_%s.so" % os.environ["PGABB_LIB_VARIANT"])
 
 u32, u64, i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
 u32p = ctypes.POINTER(ctypes.c_uint32)
