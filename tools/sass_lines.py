@@ -31,9 +31,16 @@ def line_map(cubin, kname):
 
 def main(rep, cubin, kname):
     mp = line_map(cubin, kname)
-    raw = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv"], text=True)
+    raw = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                                   "-k", f"regex:{kname}"], text=True)
     rows = list(csv.reader(io.StringIO(raw)))
-    h, data = rows[1], rows[2:]
+    hi = next(k for k, r in enumerate(rows) if r and r[0] == "Address")
+    h = rows[hi]
+    data = []
+    for r in rows[hi + 1:]:
+        if not r or r[0] in ("Kernel Name", "Address"):
+            break   # next kernel's section
+        data.append(r)
     iE, iW = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
     ins, stl = defaultdict(int), defaultdict(int)
     for k, r in enumerate(data):
