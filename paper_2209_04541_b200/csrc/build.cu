@@ -355,6 +355,20 @@ __global__ void k_row_emit(PieceDev w, const uint32_t* flags, const uint32_t* po
         if (flags[k]) out[pos[k]] = ((unsigned long long)w.task << 32) | (w.r0 + (uint32_t)k);
 }
 
+// Light items of one owned piece (16 bytes each, see internal.h).
+__global__ void k_light_emit(PieceDev w, const uint32_t* flags, const uint32_t* pos, const uint32_t* rowptr,
+                             uint4* out) {
+    const uint32_t nr = w.r1 - w.r0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nr;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        if (flags[k]) {
+            const uint32_t u = w.r0 + (uint32_t)k;
+            const uint32_t a0 = rowptr[w.rp_ix + u], la = rowptr[w.rp_ix + u + 1] - a0;
+            const uint32_t e0 = rowptr[w.rp_ij + u], le = rowptr[w.rp_ij + u + 1] - e0;
+            out[pos[k]] = make_uint4(w.task | (la << kLightTaskBits) | (le << (kLightTaskBits + 4)), a0, e0, u);
+        }
+}
+
 template <class F>
 void cub_call(F f, cudaStream_t st, DBuf<unsigned char>& tmp) {
     size_t bytes = 0;
@@ -1004,7 +1018,7 @@ void upload_work(pgabb_blocks_s* h) {
             PG_LAUNCH_CHECK();
         }
         if (piece_light[k]) {
-            k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, lf.p, lpos.p, h->d_light.p + lbase);
+            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, lf.p, lpos.p, h->d_rowptr.p, h->d_light.p + lbase);
             PG_LAUNCH_CHECK();
         }
         base += piece_items[k];

@@ -534,7 +534,7 @@ constexpr int kLightChunk = 8;   // items per lane per claim
 
 template <bool VTX>
 __global__ void __launch_bounds__(kLightThreads)
-k_tc_light(const unsigned long long* __restrict__ items, unsigned long long nitems,
+k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
            unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
@@ -550,18 +550,17 @@ k_tc_light(const unsigned long long* __restrict__ items, unsigned long long nite
     for (int r = 0; r < kLightChunk; ++r) {
         const unsigned long long idx = base + 32 * r + lane;
         if (idx >= nitems) break;
-        const unsigned long long it = __ldg(items + idx);
-        const uint32_t t = (uint32_t)(it >> 32), u = (uint32_t)it;
+        const uint4 it = __ldg(items + idx);
+        const uint32_t t = it.x & ((1u << kLightTaskBits) - 1), u = it.w;
+        const uint32_t la = (it.x >> kLightTaskBits) & 15u, a0 = it.y;
+        const uint32_t e0 = it.z, e1 = e0 + (it.x >> (kLightTaskBits + 4));
         if (t != cur_t) {
             if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
             cur_t = t;
             acc_t = 0;
         }
         const TaskDev& T = tasks[t];
-        const uint64_t rp_ix = T.rp_ix, rp_ij = T.rp_ij, col_ij = T.col_ij, bm_jx = T.bm_jx;
-        const uint32_t a0 = __ldg(rowptr + rp_ix + u), a1 = __ldg(rowptr + rp_ix + u + 1);
-        const uint32_t e0 = __ldg(rowptr + rp_ij + u), e1 = __ldg(rowptr + rp_ij + u + 1);
-        const uint32_t la = a1 - a0;
+        const uint64_t col_ij = T.col_ij, bm_jx = T.bm_jx;
         const uint32_t* __restrict__ A = col + T.col_ix + a0;
         uint32_t a[kLightLa];
 #pragma unroll

@@ -152,6 +152,13 @@ constexpr uint32_t kLightLa = 8;       // |A_ix[u]| <= 8 (the register copy)
 constexpr uint32_t kLightLe = 32;      // |A_ij[u]| <= 32 pairs
 constexpr uint32_t kLightScan = 16;
 constexpr uint32_t kLightWork = 128;   // list loads per row
+// A light item carries its row's offsets, so the kernel starts with the lists
+// instead of a chain of descriptor / rowptr loads:
+//   x = task | |A_ix[u]| << 16 | |A_ij[u]| << 20,  y = rowptr_ix[u],  z = rowptr_ij[u],  w = u
+// (task < 2^16: p <= 64 gives at most C(66,3) = 45760 tasks).
+constexpr uint32_t kLightTaskBits = 16;
+static_assert(kLightLa < 16 && kLightLe < 4096, "light item bit fields");
+static_assert((kMaxParts + 2) * (kMaxParts + 1) * kMaxParts / 6 < (1u << kLightTaskBits), "task id field");
 __host__ __device__ inline uint32_t light_pair_loads(uint32_t la, uint32_t lb) {
     if (lb <= kLightScan) return lb;
     uint32_t lg = 0;
@@ -215,7 +222,7 @@ struct pgabb_blocks_s {
     pgabb::DBuf<pgabb::TaskDev> d_tasks;             // ntasks descriptors
     pgabb::DBuf<unsigned long long> d_items;         // heavy row items (warp per row)
     uint64_t n_items = 0;
-    pgabb::DBuf<unsigned long long> d_light;         // light row items (thread per row, DESIGN R20)
+    pgabb::DBuf<uint4> d_light;                      // light row items (thread per row, DESIGN R20)
     uint64_t n_light = 0;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
