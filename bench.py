@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--cut-rule", type=int, default=0)
     ap.add_argument("--path", choices=["count", "vertex"], default="count",
                     help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1)")
+    ap.add_argument("--balance", choices=["measured", "cost"], default="measured",
+                    help="N>1: plan pieces with measured task times (R22) or the S7 cost (R17)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
@@ -254,7 +256,12 @@ def run_ours(args):
     n, s, d = cfg.generate()
     m_tuples = int(s.size)
 
-    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
+    if ws > 1 and args.balance == "measured":
+        # S8 with rank 0's measured task times broadcast to all ranks (DESIGN R22; untimed)
+        from paper_2209_04541_b200 import dist as pgd
+        b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule)
+    else:
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
     # a real (non-legacy-default) stream: the library orders its work on it and the
@@ -370,7 +377,7 @@ def run_ours(args):
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "path": args.path, "n": n, "tuples": m_tuples, "m_edges": m_edges,
                        "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
                        "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
-                       "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}",
+                       "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}", "balance": args.balance if ws > 1 else None,
                        "comm": comm.backend,
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "timer": "CUDA events per step on the launch stream, max over ranks"},

@@ -82,6 +82,17 @@ typedef struct {
     uint32_t reserved0;
     uint64_t device_budget_bytes; /* HOST residency: device bytes for staged blocks;
                                      0 = stage all of this rank's blocks at once */
+    const uint64_t* task_weights; /* optional HOST uint64[n_task_weights]: the task
+                                     estimates E(t) ("E functor if
+                                     defined"), in task order -- e.g. device time per
+                                     task measured by pgabb_task_times on one GPU and
+                                     broadcast, so that every rank plans the same
+                                     pieces.  NULL = the S7 cost (DESIGN R17).  Used
+                                     for splitting (cap = total/(4G)) and LPT; pieces
+                                     are still cut at row-cost quantiles (R22).
+                                     Borrowed for the call. */
+    uint64_t n_task_weights;      /* must equal the task count when task_weights != NULL
+                                     (EINVAL otherwise) */
 } pgabb_build_opts_t;
 
 /* Fills *opts with the defaults (p=0->8, rule 0, current device, one rank, HBM). */
@@ -177,6 +188,19 @@ typedef struct {
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);
+
+/*
+ * Measured task estimates for the scheduler (S8; the paper's E functor,
+ * PAPER.md:843-846).  Runs one count of this handle's pieces with per-task
+ * cycle accounting and writes, for every task t, its share of the measured
+ * device time in nanoseconds: ns[t] = sum over the two S10 kernels of
+ * kernel_ns * cycles_t / cycles_all (HOST uint64[ntasks]; tasks this rank does
+ * not own get 0).  Measure on a world_size-1 handle, broadcast, and pass as
+ * pgabb_build_opts_t.task_weights so every rank plans identical pieces.
+ * Device-resident handles only (EINVAL for streaming residency).
+ * Errors: EINVAL (NULL argument), ECUDA.
+ */
+PGABB_API pgabb_status_t pgabb_task_times(pgabb_blocks_t b, uint64_t* ns);
 
 /* ---- introspection (parity tests of S2..S8); all outputs are HOST buffers ---- */
 

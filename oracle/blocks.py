@@ -187,9 +187,15 @@ def task_alg_bytes(B, t) -> int:
 
 # S8 -- pieces and LPT (PAPER.md:756-757, 843-849 §4.1/§4.4 "sorts them in
 # decreasing order"; reading R18).
-def pieces(B, tasks_, costs, G: int):
-    """[(task_idx, row_begin, row_end, cost)] in (task, row) order; zero-cost dropped."""
-    total = int(sum(costs))
+def pieces(B, tasks_, costs, G: int, weights=None):
+    """[(task_idx, row_begin, row_end, weight)] in (task, row) order; zero-cost dropped.
+
+    weights (reading R22): the scheduler's task estimates E(t) (PAPER.md:843-846,
+    "E functor if defined"); None means E(t) = the S7 cost.  cap = ceil(total E /
+    (4G)); a task with E(t) > cap is cut into k = ceil(E(t)/cap) row ranges at
+    row-cost quantiles, and a range's weight is floor(E(t) * its row cost / cost)."""
+    E = [int(c) for c in costs] if weights is None else [int(w) for w in weights]
+    total = sum(E[ti] for ti in range(len(tasks_)) if int(costs[ti]) > 0)
     cap = None if G <= 1 else max(1, -(-total // (4 * G)))
     out = []
     for ti, t in enumerate(tasks_):
@@ -197,10 +203,11 @@ def pieces(B, tasks_, costs, G: int):
         cost = int(costs[ti])
         if cost == 0:
             continue
-        if cap is None or cost <= cap:
-            out.append((ti, 0, nrows, cost))
+        w = E[ti]
+        if cap is None or w <= cap:
+            out.append((ti, 0, nrows, w))
             continue
-        k = -(-cost // cap)
+        k = -(-w // cap)
         R = np.concatenate([[0], np.cumsum(row_costs(B, t))])
         bnd = [0]
         for q in range(1, k):
@@ -209,7 +216,7 @@ def pieces(B, tasks_, costs, G: int):
         for q in range(k):
             c = int(R[bnd[q + 1]] - R[bnd[q]])
             if c > 0:
-                out.append((ti, bnd[q], bnd[q + 1], c))
+                out.append((ti, bnd[q], bnd[q + 1], w * c // cost))
     return out
 
 
@@ -239,7 +246,7 @@ def piece_count(B, t, r0: int, r1: int) -> int:
 class Plan:
     """All intermediate objects of the block method for one (graph, p, rule, G)."""
 
-    def __init__(self, n, src, dst, p, rule=0, G=1):
+    def __init__(self, n, src, dst, p, rule=0, G=1, weights=None):
         self.n = int(n)
         self.E = canonical_edges(n, src, dst)
         self.deg = degrees(n, self.E)
@@ -252,7 +259,7 @@ class Plan:
         self.costs = [task_cost(self.B, t) for t in self.tasks]
         self.alg_bytes = [task_alg_bytes(self.B, t) for t in self.tasks]
         self.G = G
-        self.pieces = pieces(self.B, self.tasks, self.costs, G)
+        self.pieces = pieces(self.B, self.tasks, self.costs, G, weights)
         self.owner, self.loads = lpt(self.pieces, G)
 
     def task_counts(self):

@@ -150,6 +150,13 @@ class Blocks:
             "pgabb_local_clustering")
         return cc[:self.n]
 
+    def task_times(self) -> np.ndarray:
+        """Measured device time per task (ns, uint64[ntasks]) of this handle's pieces:
+        the scheduler's E(t) for a balanced multi-GPU plan (pgabb_task_times)."""
+        out = np.zeros(max(self.ntasks, 1), np.uint64)
+        _ck(_lib.pgabb_task_times(self._h, out.ctypes.data_as(_abi.u64p)), "pgabb_task_times")
+        return out[:self.ntasks]
+
     # --- introspection ---
     def stats(self) -> dict:
         s = _abi.Stats()
@@ -203,10 +210,13 @@ class Blocks:
 
 
 def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = -1, rank: int = 0,
-                 world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0) -> Blocks:
+                 world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0,
+                 task_weights=None) -> Blocks:
     """S1..S8: canonicalise, degree-order, orient, cut, block, enumerate, cost, assign.
 
-    src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device)."""
+    src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device).
+    task_weights: optional per-task estimates E(t) (e.g. Blocks.task_times() of a
+    1-rank handle, identical on every rank) used by S8 instead of the S7 cost."""
     sp, sn, sdev, keep_s = _pointer(src)
     dp, dn, ddev, keep_d = _pointer(dst)
     if sn != dn:
@@ -219,10 +229,15 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     o.inputs_on_device = int(sdev)
     o.rank, o.world_size, o.residency = rank, world_size, residency
     o.device_budget_bytes = device_budget_bytes
+    tw = None
+    if task_weights is not None:
+        tw = np.ascontiguousarray(task_weights, dtype=np.uint64)
+        o.task_weights = tw.ctypes.data_as(_abi.u64p)
+        o.n_task_weights = tw.size
     h = ctypes.c_void_p(0)
     st = _lib.pgabb_build_blocks(int(n), int(sn), ctypes.c_void_p(sp) if sn else None,
                                  ctypes.c_void_p(dp) if dn else None, ctypes.byref(o), ctypes.byref(h))
-    del keep_s, keep_d
+    del keep_s, keep_d, tw
     _ck(st, "pgabb_build_blocks")
     s = _abi.Stats()
     _ck(_lib.pgabb_get_stats(h, ctypes.byref(s)), "pgabb_get_stats")

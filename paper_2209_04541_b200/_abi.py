@@ -30,7 +30,7 @@ OUT_DEVICE = 2
 class BuildOpts(ctypes.Structure):
     _fields_ = [("p", u32), ("cut_rule", u32), ("device", i32), ("inputs_on_device", u32),
                 ("rank", i32), ("world_size", i32), ("residency", u32), ("reserved0", u32),
-                ("device_budget_bytes", u64)]
+                ("device_budget_bytes", u64), ("task_weights", u64p), ("n_task_weights", u64)]
 
 
 class CountOpts(ctypes.Structure):
@@ -60,6 +60,7 @@ SIGNATURES = [
     ("pgabb_vertex_triangles", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, u64p]),
     ("pgabb_local_clustering", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, vp]),
     ("pgabb_get_stats", ctypes.c_int, [vp, ctypes.POINTER(Stats)]),
+    ("pgabb_task_times", ctypes.c_int, [vp, u64p]),
     ("pgabb_get_rank", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_cuts", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_block", ctypes.c_int, [vp, u32, u32, u32p, u32p, u64p]),

@@ -141,6 +141,8 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->residency = o.residency;
         h->budget = o.device_budget_bytes;
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
+        if (o.task_weights) h->task_weights.assign(o.task_weights, o.task_weights + o.n_task_weights);
+        else if (o.n_task_weights) fail(PGABB_EINVAL, "n_task_weights > 0 with task_weights NULL");
         build_graph(h, m, src, dst, o.inputs_on_device != 0);
         plan_pieces(h);
         upload_work(h);
@@ -220,6 +222,15 @@ pgabb_status_t pgabb_local_clustering(pgabb_blocks_t b, const pgabb_count_opts_t
         if ((!tv || !cc) && b->n) fail(PGABB_EINVAL, "tv or cc is NULL");
         DeviceGuard g(b->device);
         local_clustering(b, opts, tv, cc);
+    });
+}
+
+pgabb_status_t pgabb_task_times(pgabb_blocks_t b, uint64_t* ns) {
+    return guarded([&] {
+        if (!b || !ns) fail(PGABB_EINVAL, "NULL argument");
+        if (b->streaming) fail(PGABB_EINVAL, "task times are measured on a device-resident handle");
+        DeviceGuard g(b->device);
+        task_times(b, ns);
     });
 }
 

@@ -694,19 +694,30 @@ void plan_pieces(pgabb_blocks_s* h) {
     const uint32_t p = h->p;
     const int G = std::max(1, h->world_size);
     h->pieces.clear();
-    uint64_t total = h->cost_total;
+    // E(t): the caller's task weights if given (R22), else the S7 cost (R17)
+    const bool weighted = !h->task_weights.empty();
+    if (weighted && h->task_weights.size() != h->tasks.size())
+        fail(PGABB_EINVAL, "task_weights has " + std::to_string(h->task_weights.size()) + " entries, the grid has " +
+                               std::to_string(h->tasks.size()) + " tasks");
+    auto E = [&](size_t t) -> uint64_t { return weighted ? h->task_weights[t] : h->tasks[t].cost; };
+    unsigned __int128 total128 = 0;
+    for (size_t t = 0; t < h->tasks.size(); ++t)
+        if (h->tasks[t].cost) total128 += E(t);
+    if (total128 >= ((unsigned __int128)1 << 63)) fail(PGABB_EINVAL, "task weights sum to >= 2^63");
+    const uint64_t total = (uint64_t)total128;
     const uint64_t cap = (G <= 1) ? ~0ull : std::max<uint64_t>(1, (total + 4ull * G - 1) / (4ull * G));
     DBuf<unsigned long long> rc, R;
     DBuf<unsigned char> tmp;
     for (size_t t = 0; t < h->tasks.size(); ++t) {
         const Task& T = h->tasks[t];
         const BlockInfo& bij = h->blocks[T.i * p + T.j];
-        if (T.cost == 0) continue;
-        if (T.cost <= cap) {
-            h->pieces.push_back(Piece{(uint32_t)t, 0, bij.nrows, T.cost, 0});
+        if (T.cost == 0) continue;   // no (u,v,x) with a non-empty list: count 0
+        const uint64_t w = E(t);
+        if (w <= cap) {
+            h->pieces.push_back(Piece{(uint32_t)t, 0, bij.nrows, w, 0, T.cost});
             continue;
         }
-        const uint64_t k = (T.cost + cap - 1) / cap;
+        const uint64_t k = (w + cap - 1) / cap;
         const uint32_t nr = bij.nrows;
         rc.alloc((size_t)nr + 1);
         R.alloc((size_t)nr + 1);
@@ -735,7 +746,9 @@ void plan_pieces(pgabb_blocks_s* h) {
         bnd.push_back(nr);
         for (uint64_t q = 0; q < k; ++q) {
             const uint64_t c = hR[bnd[q + 1]] - hR[bnd[q]];
-            if (c > 0) h->pieces.push_back(Piece{(uint32_t)t, bnd[q], bnd[q + 1], c, 0});
+            // piece weight: w * (its row-cost share), floor; = c when w is the S7 cost
+            const uint64_t pw = weighted ? (uint64_t)((unsigned __int128)w * c / T.cost) : c;
+            if (c > 0) h->pieces.push_back(Piece{(uint32_t)t, bnd[q], bnd[q + 1], pw, 0, c});
         }
     }
     // LPT: heaviest first (ties: task, row), least-loaded rank (ties: lowest rank)
@@ -904,7 +917,7 @@ void upload_work(pgabb_blocks_s* h) {
         const Task& T = h->tasks[t];
         uint64_t mine = 0;
         for (const Piece& pc : h->pieces)
-            if (pc.task == t && pc.owner == me) mine += pc.cost;
+            if (pc.task == t && pc.owner == me) mine += pc.rcost;
         h->alg_local += (uint64_t)((long double)T.alg_bytes * mine / (T.cost ? T.cost : 1));
     }
     h->d_work.alloc(std::max<size_t>(h->work.size(), 1));

@@ -388,13 +388,14 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
 // VTX = true (per-vertex counts, NEXT-1): tv[rank-space id] += the triangles
 // found here that contain the vertex -- u gets the row total, v each pair's
 // c_uv, w one per hit -- so sum over ranks of tv = t(v) and sum tv = 3T.
-template <bool IMPLICIT, bool VTX>
+// TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
+template <bool IMPLICIT, bool VTX, bool TIMED>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
           unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
-          unsigned long long* __restrict__ next) {
+          unsigned long long* __restrict__ next, unsigned long long* __restrict__ cyc) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -429,6 +430,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             t = (uint32_t)(it >> 32);
             u = (uint32_t)it;
         }
+        const long long c0 = TIMED ? clock64() : 0;
         const TaskDev T = tasks[t];
         const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
         const uint32_t e0 = __ldg(rowptr + T.rp_ij + u), e1 = __ldg(rowptr + T.rp_ij + u + 1);
@@ -501,6 +503,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             atomicAdd(&task_counts[t], (unsigned long long)sum);
             if (VTX) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
         }
+        if (TIMED && lane == 0) atomicAdd(&cyc[t], (unsigned long long)(clock64() - c0));
         PROF_MARK(7);
     }
 #ifdef PGABB_PROF
@@ -532,16 +535,16 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 constexpr int kLightThreads = 256;
 constexpr int kLightChunk = 8;   // items per lane per claim
 
-template <bool VTX>
+template <bool VTX, bool TIMED>
 __global__ void __launch_bounds__(kLightThreads)
 k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
            unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
-           unsigned long long* __restrict__ next) {
+           unsigned long long* __restrict__ next, unsigned long long* __restrict__ cyc) {
     const int lane = threadIdx.x & 31;
     uint32_t cur_t = 0xffffffffu;
-    unsigned long long acc_t = 0;
+    unsigned long long acc_t = 0, cyc_t = 0;
     for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(next, (unsigned long long)(32 * kLightChunk));
@@ -556,9 +559,12 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
         const uint32_t e0 = it.z, e1 = e0 + (it.x >> (kLightTaskBits + 4));
         if (t != cur_t) {
             if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+            if (TIMED && cyc_t) atomicAdd(&cyc[cur_t], cyc_t);
             cur_t = t;
             acc_t = 0;
+            cyc_t = 0;
         }
+        const long long c0 = TIMED ? clock64() : 0;
         const TaskDev& T = tasks[t];
         const uint64_t col_ij = T.col_ij, bm_jx = T.bm_jx;
         const uint32_t* __restrict__ A = col + T.col_ix + a0;
@@ -622,9 +628,11 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
         }
         acc_t += acc;
         if (VTX && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
+        if (TIMED) cyc_t += (unsigned long long)(clock64() - c0);
     }
     }
     if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+    if (TIMED && cyc_t) atomicAdd(&cyc[cur_t], cyc_t);
 }
 
 // S11: T_rank = sum of the per-task counts (written after them, at [ntasks]).
@@ -693,7 +701,8 @@ namespace pgabb {
 #endif
 
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
-                         unsigned long long* d_tv_out) {
+                         unsigned long long* d_tv_out, unsigned long long* d_cycles) {
+    const bool timed = d_cycles != nullptr;   // pgabb_task_times: counting kernels with cycle accounting
     cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
     const bool async = opts && (opts->flags & PGABB_COUNT_ASYNC);
     const int nt = (int)h->tasks.size();
@@ -707,15 +716,16 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     if (cached_dev != h->device) {
         const size_t sm_c = kRowWarps * (kSetWords + scratch_words(false)) * sizeof(uint32_t);
         const size_t sm_v = kRowWarps * (kSetWords + scratch_words(true)) * sizeof(uint32_t);
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
+        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
         int sms = 0, per_sm = 0;
         PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, false>, kRowWarps * 32, sm_c));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, false, false>, kRowWarps * 32, sm_c));
         grid_c = sms * std::max(per_sm, 1);
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, true>, kRowWarps * 32, sm_v));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, true, false>, kRowWarps * 32, sm_v));
         grid_v = sms * std::max(per_sm, 1);
         cached_dev = h->device;
     }
@@ -730,8 +740,9 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         tv = h->d_tv_rank.p;
     }
     auto rows_kernel = [&](bool implicit) {
-        if (implicit) return vtx ? k_tc_rows<true, true> : k_tc_rows<true, false>;
-        return vtx ? k_tc_rows<false, true> : k_tc_rows<false, false>;
+        if (implicit) return vtx ? k_tc_rows<true, true, false> : k_tc_rows<true, false, false>;
+        if (timed) return k_tc_rows<false, false, true>;
+        return vtx ? k_tc_rows<false, true, false> : k_tc_rows<false, false, false>;
     };
 
     PG_CK(cudaEventRecord(h->ev0, st));
@@ -750,7 +761,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         if (h->n_items) {
             rows_kernel(false)<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
                 h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p, tv, h->d_next.p + 1);
+                h->d_task_counts.p, tv, h->d_next.p + 1, d_cycles);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -761,15 +772,16 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             if (light_dev != h->device) {
                 int sms = 0, per_sm = 0;
                 PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false>, kLightThreads, 0));
+                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false, false>, kLightThreads, 0));
                 light_grid = sms * std::max(per_sm, 1);
                 light_dev = h->device;
             }
             const unsigned g = (unsigned)std::max<unsigned long long>(
                 1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
-            (vtx ? k_tc_light<true> : k_tc_light<false>)<<<g, kLightThreads, 0, st>>>(
-                h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p, tv, h->d_next.p);
+            (timed ? k_tc_light<false, true> : vtx ? k_tc_light<true, false> : k_tc_light<false, false>)
+                <<<g, kLightThreads, 0, st>>>(h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p,
+                                              h->d_bitmap.p, h->d_task_counts.p, tv, h->d_next.p,
+                                              timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -796,7 +808,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             const uint32_t* base = h->d_arena[a].p;
             rows_kernel(true)<<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
                 nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, nullptr);
+                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, nullptr, nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
             PG_CK(cudaEventRecord(h->ev_done[a], st));
@@ -827,6 +839,31 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     }
     *wrote = true;
     return h->h_result.p[0];
+}
+
+void task_times(pgabb_blocks_s* h, uint64_t* ns) {
+    const size_t nt = h->tasks.size();
+    if (nt == 0) return;
+    DBuf<unsigned long long> cyc;
+    cyc.alloc(2 * nt);
+    PG_CK(cudaMemsetAsync(cyc.p, 0, 2 * nt * 8, h->stream));
+    bool wrote = false;
+    count_triangles(h, nullptr, &wrote, nullptr, cyc.p);
+    std::vector<unsigned long long> c(2 * nt);
+    PG_CK(cudaMemcpy(c.data(), cyc.p, 2 * nt * 8, cudaMemcpyDeviceToHost));
+    long double sh = 0, sl = 0;
+    for (size_t t = 0; t < nt; ++t) {
+        sh += c[t];
+        sl += c[nt + t];
+    }
+    const long double ns_h = 1e6L * std::max(0.0, h->ms_main_last - h->ms_light_last);
+    const long double ns_l = 1e6L * h->ms_light_last;
+    for (size_t t = 0; t < nt; ++t) {
+        long double v = 0;
+        if (sh > 0) v += ns_h * c[t] / sh;
+        if (sl > 0) v += ns_l * c[nt + t] / sl;
+        ns[t] = (uint64_t)(v + 0.5L);
+    }
 }
 
 void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc) {

@@ -106,8 +106,9 @@ struct Task {
 struct Piece {
     uint32_t task;
     uint32_t r0, r1;         // local rows of part i
-    uint64_t cost;
+    uint64_t cost;           // scheduling weight (S7 cost range, or the task weight's share, R22)
     int32_t owner;
+    uint64_t rcost = 0;      // S7 row-cost range of the piece (for the bytes attribution)
 };
 
 // Work-list entry for the intersection kernels (one per owned piece).
@@ -206,6 +207,7 @@ struct pgabb_blocks_s {
     std::vector<pgabb::Task> tasks;             // (i,j,x) lexicographic
     std::vector<pgabb::Piece> pieces;           // (task, row) order
     std::vector<uint32_t> task_of_ijx;          // p^3 -> task id or kNoTask
+    std::vector<uint64_t> task_weights;         // caller's E(t) (empty: the S7 cost)
 
     pgabb::DBuf<uint32_t> d_rank;               // original id -> rank
     pgabb::DBuf<uint32_t> d_deg;                // original id -> degree in G_s (S2; clustering)
@@ -257,7 +259,8 @@ void plan_pieces(pgabb_blocks_s* h);
 void upload_work(pgabb_blocks_s* h);
 void plan_waves(pgabb_blocks_s* h);
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
-                         unsigned long long* d_tv_out = nullptr);
+                         unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr);
+void task_times(pgabb_blocks_s* h, uint64_t* ns);
 void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc);
 void resolve_timing(pgabb_blocks_s* h);
 }  // namespace pgabb

@@ -67,3 +67,36 @@ def combine_vertex_counts_host(local, group=None):
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.numpy().astype(np.uint64)
+
+
+def build_blocks_balanced(n, src, dst, p=0, cut_rule=0, group=None, **kw):
+    """S8 with measured task estimates (DESIGN R22): rank 0 times every task on a
+    1-rank handle (pgabb_task_times), broadcasts the per-task nanoseconds, and
+    every rank plans its LPT share with them -- the same plan everywhere, balanced
+    by device time instead of the S7 merge cost.  Untimed pre-processing."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    ws = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    if ws <= 1:
+        return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, **kw)
+    with build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev) as b1:
+        ns = b1.task_times() if rank == 0 else np.zeros(b1.ntasks, np.uint64)
+    w = broadcast_weights(ns, group)
+    return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,
+                        task_weights=w, **kw)
+
+
+def broadcast_weights(ns, group=None):
+    """Rank 0's per-task estimates to every rank (int64 over the group's backend)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(ns, dtype=np.uint64).astype(np.int64))
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+    return t.cpu().numpy().astype(np.uint64)

@@ -212,3 +212,40 @@ def test_pieces_lpt_and_rank_sum(G):
             assert T_r == want
             total += T_r
     assert total == oracle.count(*g)
+
+
+# ---------------------------------------------------------------- S8 with task weights (R22)
+@pytest.mark.parametrize("G", [2, 4])
+def test_weighted_pieces_and_rank_sum(G):
+    g = gen.rmat(11, 16, seed=22)
+    with pg.build_blocks(*g, p=5) as b1:
+        nt = b1.ntasks
+    rng = np.random.default_rng(G)
+    w = rng.integers(0, 10 ** 9, nt).astype(np.uint64)
+    P = ob.Plan(*g, p=5, G=G, weights=[int(x) for x in w])
+    total = 0
+    for r in range(G):
+        with pg.build_blocks(*g, p=5, rank=r, world_size=G, task_weights=w) as b:
+            pcs, owner = b.pieces()
+            assert pcs == P.pieces and owner == P.owner
+            total += b.triangle_count()
+    assert total == oracle.count(*g)
+
+
+def test_task_times_drive_a_balanced_plan():
+    g = gen.rmat(14, 16, seed=23)
+    with pg.build_blocks(*g, p=8) as b1:
+        ns = b1.task_times()
+        st = b1.stats()
+        T1 = b1.triangle_count()
+    assert ns.shape == (b1.ntasks,) and ns.sum() > 0
+    # the estimates add up to the measured kernel time (ns), up to rounding
+    assert abs(int(ns.sum()) - 1e6 * st["ms_main_kernel_last"]) <= 1e6 * st["ms_main_kernel_last"] * 0.01 + b1.ntasks
+    total = 0
+    for r in range(4):
+        with pg.build_blocks(*g, p=8, rank=r, world_size=4, task_weights=ns) as b:
+            total += b.triangle_count()
+    assert total == T1 == oracle.count(*g)
+    with pytest.raises(pg.PgabbError) as e:
+        pg.build_blocks(*g, p=8, task_weights=ns[:-1])
+    assert e.value.name == "EINVAL"

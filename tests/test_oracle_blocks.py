@@ -215,6 +215,39 @@ def test_pieces_k4_hand():
     assert P.loads == [12, 6]
 
 
+def test_weighted_pieces_k4_hand():
+    # E = [36] (reading R22): cap = ceil(36/8) = 5, k = ceil(36/5) = 8; boundaries
+    # rho_q = min{rho : 8 R[rho] >= 18 q}, R = [0,12,17,18,18] -> q=1..5: 1, q=6,7: 2.
+    # Ranges [0,1) c=12, [1,2) c=5, [2,4) c=1; weights floor(36 c / 18) = 24, 10, 2.
+    P = ob.Plan(*gen.complete(4), p=1, G=2, weights=[36])
+    assert P.pieces == [(0, 0, 1, 24), (0, 1, 2, 10), (0, 2, 4, 2)]
+    assert P.owner == [0, 1, 1] and P.loads == [24, 12]
+
+
+def test_weights_equal_to_costs_change_nothing():
+    g = gen.rmat(9, 16, seed=3)
+    for G in (1, 2, 5):
+        A = ob.Plan(*g, p=4, G=G)
+        B = ob.Plan(*g, p=4, G=G, weights=A.costs)
+        assert A.pieces == B.pieces and A.owner == B.owner
+
+
+def test_weights_steer_lpt():
+    # two equal-cost tasks made unequal by E: the heavier one gets a rank of its own
+    g = gen.rmat(9, 16, seed=4)
+    A = ob.Plan(*g, p=3, G=3)
+    w = [0] * len(A.tasks)
+    heavy = int(np.argmax(A.costs))
+    w[heavy] = 10 ** 12
+    B = ob.Plan(*g, p=3, G=3, weights=w)
+    owners_heavy = {o for pc, o in zip(B.pieces, B.owner) if pc[0] == heavy}
+    owners_rest = {o for pc, o in zip(B.pieces, B.owner) if pc[0] != heavy}
+    # E of the heavy task is above the cap: it is split over all ranks; every task is still assigned
+    assert len(owners_heavy) == 3
+    assert {pc[0] for pc in B.pieces} == {t for t, c in enumerate(A.costs) if c > 0}
+    assert owners_rest
+
+
 def test_lpt_hand():
     pcs = [(0, 0, 1, 5), (1, 0, 1, 4), (2, 0, 1, 3), (3, 0, 1, 3), (4, 0, 1, 3)]
     owner, loads = ob.lpt(pcs, 2)
