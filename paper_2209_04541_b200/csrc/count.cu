@@ -94,8 +94,33 @@ __device__ __forceinline__ unsigned long long claim_items(unsigned long long* ne
 constexpr int kRowMinBlocks = 5;   // = the shared-memory limit (5 x 8 warps x 4.4 KB)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
 constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
-constexpr uint32_t kScratchWordsV = 128;                 // + the batch's v ids (per-vertex kernel)
+// per-vertex kernel: + the batch's v ids (32), the row's prefix popcounts of S
+// (1024 u16) and its hit counters (1024 u16), see VCnt
+constexpr uint32_t kVtxSlots = 1024;
+constexpr uint32_t kScratchWordsV = 128 + kVtxSlots / 2 + kVtxSlots / 2;
 __host__ __device__ constexpr uint32_t scratch_words(bool vtx) { return vtx ? kScratchWordsV : kScratchWords; }
+
+// Per-vertex counts, third vertex w (NEXT-1): a hub w is hit by many v of the same
+// row, so instead of one global atomic per hit the row's hits are counted in warp
+// shared memory -- u16 counters indexed by w's position in A_ix[u] (bitmap set:
+// rank of w = prefix popcount of S, kept per word in pre) or by w's hash slot --
+// and flushed with one atomic per distinct w at the end of the row.  on = false
+// (|A_ix[u]| > kVtxSlots, |A_ij[u]| >= 2^16, or the search fallback) means one
+// global atomic per hit.
+struct VCnt {
+    uint32_t* cnt;                     // u16 x kVtxSlots, packed in pairs
+    uint32_t* pre;                     // u16 x kVtxSlots: popcount of S[0..k) (bitmap mode)
+    unsigned long long* tvx;           // global t(v) of part x
+    bool on;
+};
+__device__ __forceinline__ void vcnt_add(uint32_t* cnt, uint32_t idx) {
+    atomicAdd(&cnt[idx >> 1], 1u << ((idx & 1u) << 4));
+}
+__device__ __forceinline__ uint32_t u16_at(const uint32_t* a, uint32_t k) { return (a[k >> 1] >> ((k & 1u) << 4)) & 0xffffu; }
+// rank of w (a member of the bitmap set S) among the set's elements
+__device__ __forceinline__ uint32_t rank_in_set(const uint32_t* S, const uint32_t* pre, uint32_t w) {
+    return u16_at(pre, w >> 5) + __popc(S[w >> 5] & ((1u << (w & 31)) - 1u));
+}
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
     return (w * 2654435761u) >> (32 - hbits);
@@ -107,6 +132,23 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
     uint32_t h = hash_slot(w, hbits), s;
     while ((s = S[h]) != 0u && s != w + 1) h = (h + 1) & hmask;
     return s == w + 1;
+}
+
+// hash mode: the slot holding w (w a member), for the per-vertex counters
+__device__ __forceinline__ uint32_t hash_find(const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask) {
+    uint32_t h = hash_slot(w, hbits);
+    while (S[h] != w + 1) h = (h + 1) & hmask;
+    return h;
+}
+
+// one hit on w (a member of the staged set S of the row)
+template <int MODE>
+__device__ __forceinline__ void vhit(const VCnt& vc, const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask) {
+    if (!vc.on) {
+        atomicAdd(vc.tvx + w, 1ull);
+        return;
+    }
+    vcnt_add(vc.cnt, MODE == 0 ? rank_in_set(S, vc.pre, w) : hash_find(S, w, hbits, hmask));
 }
 
 // One row u: every v in A_ij[u] (edges e0..e1), 32 at a time (one per lane).
@@ -129,26 +171,26 @@ __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_
 // in v's sorted list instead of streaming the whole list.
 // Components c of x with lo <= c < hi (the part of a 16-byte vector inside a list)
 // probed against S.
-// VTX: a hit on w also adds 1 to tvx[w] (the triangle's third vertex).
+// VTX: a hit on w is also counted for w (the triangle's third vertex).
 template <int MODE, bool VTX>
 __device__ __forceinline__ uint32_t probe1(const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask,
-                                           unsigned long long* __restrict__ tvx) {
+                                           const VCnt& vc) {
     const uint32_t h = probe<MODE>(S, w, hbits, hmask);
-    if (VTX && h) atomicAdd(tvx + w, 1ull);
+    if (VTX && h) vhit<MODE>(vc, S, w, hbits, hmask);
     return h;
 }
 
 template <int MODE, bool VTX>
 __device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int lo, int hi, uint32_t hbits,
-                                           uint32_t hmask, unsigned long long* __restrict__ tvx) {
+                                           uint32_t hmask, const VCnt& vc) {
     if (lo <= 0 && hi >= 4)
-        return probe1<MODE, VTX>(S, x.x, hbits, hmask, tvx) + probe1<MODE, VTX>(S, x.y, hbits, hmask, tvx) +
-               probe1<MODE, VTX>(S, x.z, hbits, hmask, tvx) + probe1<MODE, VTX>(S, x.w, hbits, hmask, tvx);
+        return probe1<MODE, VTX>(S, x.x, hbits, hmask, vc) + probe1<MODE, VTX>(S, x.y, hbits, hmask, vc) +
+               probe1<MODE, VTX>(S, x.z, hbits, hmask, vc) + probe1<MODE, VTX>(S, x.w, hbits, hmask, vc);
     uint32_t c = 0;
-    if (lo <= 0 && 0 < hi) c += probe1<MODE, VTX>(S, x.x, hbits, hmask, tvx);
-    if (lo <= 1 && 1 < hi) c += probe1<MODE, VTX>(S, x.y, hbits, hmask, tvx);
-    if (lo <= 2 && 2 < hi) c += probe1<MODE, VTX>(S, x.z, hbits, hmask, tvx);
-    if (lo <= 3 && 3 < hi) c += probe1<MODE, VTX>(S, x.w, hbits, hmask, tvx);
+    if (lo <= 0 && 0 < hi) c += probe1<MODE, VTX>(S, x.x, hbits, hmask, vc);
+    if (lo <= 1 && 1 < hi) c += probe1<MODE, VTX>(S, x.y, hbits, hmask, vc);
+    if (lo <= 2 && 2 < hi) c += probe1<MODE, VTX>(S, x.z, hbits, hmask, vc);
+    if (lo <= 3 && 3 < hi) c += probe1<MODE, VTX>(S, x.w, hbits, hmask, vc);
     return c;
 }
 
@@ -165,7 +207,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                                                   uint32_t* __restrict__ scratch, uint32_t hbits, uint32_t hmask,
                                                   const uint32_t* __restrict__ A, uint32_t la, int lane,
                                                   unsigned long long* __restrict__ tvj,
-                                                  unsigned long long* __restrict__ tvx PROF_ARGS) {
+                                                  const VCnt& vc PROF_ARGS) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     const uint32_t le_mask = 0xffffffffu >> (31 - lane);
     uint32_t gsz = 1;
@@ -210,14 +252,14 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                                 cv += __popc(wd);
                                 if (VTX)
                                     for (; wd; wd &= wd - 1u)
-                                        atomicAdd(tvx + 32u * (kl + r * 32) + (__ffs(wd) - 1), 1ull);
+                                        vhit<0>(vc, S, 32u * (kl + r * 32) + (__ffs(wd) - 1), 0, 0);
                             }
                     } else {
                         for (uint32_t k = kl; k < W; k += gsz) {
                             uint32_t wd = S[k] & __ldg(row + (k - kl));
                             cv += __popc(wd);
                             if (VTX)
-                                for (; wd; wd &= wd - 1u) atomicAdd(tvx + 32u * k + (__ffs(wd) - 1), 1ull);
+                                for (; wd; wd &= wd - 1u) vhit<0>(vc, S, 32u * k + (__ffs(wd) - 1), 0, 0);
                         }
                     }
                     acc += cv;
@@ -243,7 +285,10 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                             if (__ldg(Bc + b0 + mid) < ak) lo = mid + 1; else hi = mid;
                         }
                         const uint32_t hit = (lo < lb && __ldg(Bc + b0 + lo) == ak);
-                        if (VTX && hit) atomicAdd(tvx + ak, 1ull);
+                        if (VTX && hit) {
+                            if (vc.on) vcnt_add(vc.cnt, MODE == 0 ? c + k : hash_find(S, ak, hbits, hmask));
+                            else atomicAdd(vc.tvx + ak, 1ull);
+                        }
                         cv += hit;
                     }
                 }
@@ -309,7 +354,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int w0 = 4 * (int)vpos[r];
-                const uint32_t c = probe4<MODE, VTX>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, tvx);
+                const uint32_t c = probe4<MODE, VTX>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, vc);
                 acc += c;
                 if (VTX && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
             }
@@ -340,14 +385,18 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
         const uint32_t P = ne * la;
         for (uint32_t base = 0; base < P; base += 32) {
             const uint32_t v = __shfl_sync(0xffffffffu, vq, q & 31);
+            uint32_t hit = 0, a = 0;
             if (base + lane < P) {
-                const uint32_t a = __ldg(A + k);
-                const uint32_t hit = (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
-                if (VTX && hit) {
-                    atomicAdd(tvx + a, 1ull);
+                a = __ldg(A + k);
+                hit = (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
+                acc += hit;
+            }
+            if (VTX) {   // lanes hitting the same w add once (warp-aggregated)
+                const uint32_t same = __match_any_sync(0xffffffffu, hit ? a : 0xffffffffu);
+                if (hit) {
+                    if (lane == __ffs(same) - 1) atomicAdd(tvx + a, (unsigned long long)__popc(same));
                     atomicAdd(tvj + v, 1ull);
                 }
-                acc += hit;
             }
             q += dq;
             k += dk;
@@ -368,10 +417,11 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
             const uint32_t m = min(32u, la - c);
             for (uint32_t k = 0; k < m; ++k) {
                 const uint32_t ak = __shfl_sync(0xffffffffu, a, k);
-                if (ok) {
-                    const uint32_t hit = (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u;
-                    if (VTX && hit) atomicAdd(tvx + ak, 1ull);
-                    cv += hit;
+                const uint32_t hit = ok ? (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u : 0u;
+                cv += hit;
+                if (VTX) {   // one atomic per element for the whole warp's v's
+                    const uint32_t m = __ballot_sync(0xffffffffu, hit);
+                    if (lane == 0 && m) atomicAdd(tvx + ak, (unsigned long long)__popc(m));
                 }
             }
         }
@@ -401,7 +451,11 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     const int wid = threadIdx.x >> 5;
     uint32_t* S = smem + wid * (kSetWords + scratch_words(VTX));
     uint32_t* scratch = S + kSetWords;
+    uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt)
+    uint32_t* vcnt = vpre + kVtxSlots / 2;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
+    if (VTX)
+        for (uint32_t k = lane; k < kVtxSlots / 2; k += 32) vcnt[k] = 0;   // invariant: zero between rows
     __syncwarp();
     const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
     // IMPLICIT: items dealt cyclically.  Otherwise warps claim kRowChunk items at a
@@ -447,6 +501,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         uint32_t acc = 0;
         unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
         unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
+        VCnt vc{vcnt, vpre, tvx, false};
         PROF_MARK(0);
         if (T.bm_jx != ~0ull && la <= 2 * T.bm_words) {
             acc = probe_dense_row<VTX>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
@@ -458,18 +513,47 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 atomicOr(&S[w >> 5], 1u << (w & 31));
             }
             __syncwarp();
+            if (VTX && la <= kVtxSlots && e1 - e0 < 65536u) {
+                // prefix popcounts of S per word (u16): rank of a member w = pre[w>>5] + popc below it
+                vc.on = true;
+                const uint32_t W = (T.wx + 31) / 32;
+                uint16_t* pre16 = reinterpret_cast<uint16_t*>(vpre);
+                uint32_t run = 0;
+                for (uint32_t b = 0; b < W; b += 32) {
+                    const uint32_t k = b + lane;
+                    const uint32_t c = k < W ? __popc(S[k]) : 0u;
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (k < W) pre16[k] = (uint16_t)(run + incl - c);
+                    run += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                __syncwarp();
+            }
             PROF_MARK(2);
             PROF_CNT(17);
             if (T.bm_jx != ~0ull) {
                 const uint32_t* BM = bitmap + T.bm_jx;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = intersect_row<0, 1, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
-                else if (W <= 128) acc = intersect_row<0, 4, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
-                else acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
+                if (W <= 32) acc = intersect_row<0, 1, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else if (W <= 128) acc = intersect_row<0, 4, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             } else {
-                acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, tvx PROF_PASS);
+                acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             }
             __syncwarp();
+            if (VTX && vc.on) {   // flush the row's w counters: one atomic per distinct w
+                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
+                for (uint32_t k = lane; k < la; k += 32) {
+                    const uint32_t c = c16[k];
+                    if (c) atomicAdd(tvx + __ldg(A + k), (unsigned long long)c);
+                }
+                __syncwarp();
+                for (uint32_t k = lane; k < (la + 1) / 2; k += 32) vcnt[k] = 0u;
+            }
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
         } else if (mode == 1) {
             for (uint32_t k = lane; k < la; k += 32) {
@@ -478,10 +562,20 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
+            if (VTX) vc.on = e1 - e0 < 65536u;   // slots <= 2 * kHashMaxList = kVtxSlots
             PROF_MARK(2);
             PROF_CNT(18);
-            acc = intersect_row<1, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, tvx PROF_PASS);
+            acc = intersect_row<1, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
             __syncwarp();
+            if (VTX && vc.on) {
+                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
+                for (uint32_t k = lane; k <= hmask; k += 32) {
+                    const uint32_t c = c16[k];
+                    if (c) atomicAdd(tvx + (S[k] - 1u), (unsigned long long)c);
+                }
+                __syncwarp();
+                for (uint32_t k = lane; k < (hmask + 1) / 2; k += 32) vcnt[k] = 0u;
+            }
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
             for (uint32_t e = e0; e < e1; ++e) {
