@@ -80,7 +80,10 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
 // first) and are dealt cyclically to the warps of the grid (no atomics).
 // ---------------------------------------------------------------------------
 constexpr int kRowWarps = 8;
-constexpr int kRowChunk = 4;       // row items per warp claim
+#ifndef PGABB_ROW_CHUNK
+#define PGABB_ROW_CHUNK 4
+#endif
+constexpr int kRowChunk = PGABB_ROW_CHUNK;   // row items per warp claim
 
 // Claims the next kRowChunk items for the calling warp; returns the first (>= n: done).
 __device__ __forceinline__ unsigned long long claim_items(unsigned long long* next, unsigned long long n, int lane,
@@ -627,7 +630,10 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 // k_tc_rows (Listing 5).
 // ---------------------------------------------------------------------------
 constexpr int kLightThreads = 256;
-constexpr int kLightChunk = 8;   // items per lane per claim
+#ifndef PGABB_LIGHT_CHUNK
+#define PGABB_LIGHT_CHUNK 8
+#endif
+constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
 
 template <bool VTX, bool TIMED>
 __global__ void __launch_bounds__(kLightThreads)
