@@ -80,6 +80,14 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
 // first) and are dealt cyclically to the warps of the grid (no atomics).
 // ---------------------------------------------------------------------------
 constexpr int kRowWarps = 8;
+#ifndef PGABB_AND_UNROLL
+#define PGABB_AND_UNROLL 2
+#endif
+constexpr int kAndUnroll = PGABB_AND_UNROLL;   // v rows in flight per lane group in the dense AND path
+#ifndef PGABB_DENSE_UNROLL
+#define PGABB_DENSE_UNROLL 4
+#endif
+constexpr int kDenseUnroll = PGABB_DENSE_UNROLL;   // bit tests in flight per lane in probe_dense_row
 #ifndef PGABB_ROW_CHUNK
 #define PGABB_ROW_CHUNK 4
 #endif
@@ -241,23 +249,39 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             if (use_and) scratch[32 + __popc(and_mask & lt_mask)] = v;
             __syncwarp();
             const uint32_t na = __popc(and_mask);
-            for (uint32_t q = 0; q < na; q += G) {
-                const uint32_t qq = q + g;
-                if (qq < na) {
-                    const uint32_t vq = scratch[32 + qq];
-                    const uint32_t* __restrict__ row = BM + (uint64_t)vq * W + kl;
+            // kAndUnroll v's per group per step: their row words are loaded before
+            // any is used, so that many loads are in flight per lane
+            constexpr int U = R > 0 ? kAndUnroll : 1;
+            for (uint32_t q = 0; q < na; q += U * G) {
+                uint32_t vqs[U], wds[U][R > 0 ? R : 1];
+#pragma unroll
+                for (int z = 0; z < U; ++z) {
+                    const uint32_t qq = q + z * G + g;
+                    vqs[z] = qq < na ? scratch[32 + qq] : 0xffffffffu;
+                    if (R > 0) {
+                        const uint32_t* __restrict__ row = BM + (uint64_t)(qq < na ? vqs[z] : 0u) * W + kl;
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            wds[z][r] = (qq < na && kl + r * 32 < W) ? __ldg(row + r * 32) : 0u;
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < U; ++z) {
+                    if (vqs[z] == 0xffffffffu) continue;
+                    const uint32_t vq = vqs[z];
                     uint32_t cv = 0;
                     if (R > 0) {
 #pragma unroll
-                        for (int r = 0; r < R; ++r)
-                            if (kl + r * 32 < W) {
-                                uint32_t wd = su[r] & __ldg(row + r * 32);
-                                cv += __popc(wd);
-                                if (VTX)
-                                    for (; wd; wd &= wd - 1u)
-                                        vhit<0>(vc, S, 32u * (kl + r * 32) + (__ffs(wd) - 1), 0, 0);
-                            }
+                        for (int r = 0; r < R; ++r) {
+                            uint32_t wd = su[r] & wds[z][r];
+                            cv += __popc(wd);
+                            if (VTX)
+                                for (; wd; wd &= wd - 1u)
+                                    vhit<0>(vc, S, 32u * (kl + r * 32) + (__ffs(wd) - 1), 0, 0);
+                        }
                     } else {
+                        const uint32_t* __restrict__ row = BM + (uint64_t)vq * W + kl;
+#pragma unroll 4
                         for (uint32_t k = kl; k < W; k += gsz) {
                             uint32_t wd = S[k] & __ldg(row + (k - kl));
                             cv += __popc(wd);
@@ -418,13 +442,20 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
         for (uint32_t c = 0; c < la; c += 32) {
             const uint32_t a = (c + lane < la) ? __ldg(A + c + lane) : 0u;
             const uint32_t m = min(32u, la - c);
-            for (uint32_t k = 0; k < m; ++k) {
-                const uint32_t ak = __shfl_sync(0xffffffffu, a, k);
-                const uint32_t hit = ok ? (__ldg(row + (ak >> 5)) >> (ak & 31)) & 1u : 0u;
-                cv += hit;
-                if (VTX) {   // one atomic per element for the whole warp's v's
-                    const uint32_t m = __ballot_sync(0xffffffffu, hit);
-                    if (lane == 0 && m) atomicAdd(tvx + ak, (unsigned long long)__popc(m));
+            for (uint32_t k = 0; k < m; k += kDenseUnroll) {
+                uint32_t ak[kDenseUnroll], wv[kDenseUnroll];
+#pragma unroll
+                for (int z = 0; z < kDenseUnroll; ++z) ak[z] = __shfl_sync(0xffffffffu, a, (k + z) & 31);
+#pragma unroll
+                for (int z = 0; z < kDenseUnroll; ++z) wv[z] = (ok && k + z < m) ? __ldg(row + (ak[z] >> 5)) : 0u;
+#pragma unroll
+                for (int z = 0; z < kDenseUnroll; ++z) {
+                    const uint32_t hit = (wv[z] >> (ak[z] & 31)) & 1u;
+                    cv += hit;
+                    if (VTX && k + z < m) {   // one atomic per element for the whole warp's v's
+                        const uint32_t mk = __ballot_sync(0xffffffffu, hit);
+                        if (lane == 0 && mk) atomicAdd(tvx + ak[z], (unsigned long long)__popc(mk));
+                    }
                 }
             }
         }
