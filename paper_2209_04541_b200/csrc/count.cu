@@ -661,13 +661,16 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 // k_tc_rows (Listing 5).
 // ---------------------------------------------------------------------------
 constexpr int kLightThreads = 256;
+#ifndef PGABB_LIGHT_MINB
+#define PGABB_LIGHT_MINB 8   // 8 x 256 threads per SM (32 registers): measured best on c3
+#endif
 #ifndef PGABB_LIGHT_CHUNK
 #define PGABB_LIGHT_CHUNK 8
 #endif
 constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
 
 template <bool VTX, bool TIMED>
-__global__ void __launch_bounds__(kLightThreads)
+__global__ void __launch_bounds__(kLightThreads, PGABB_LIGHT_MINB)
 k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,

@@ -149,7 +149,10 @@ constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
 // Light rows (DESIGN R20): handled one per thread by k_tc_light, A_ix[u] held in
 // registers.  A v list of <= kLightScan ids is scanned (each id compared with all
 // of A_ix[u]); a longer one is binary-searched once per element of A_ix[u].
-constexpr uint32_t kLightLa = 8;       // |A_ix[u]| <= 8 (the register copy)
+#ifndef PGABB_LIGHT_LA
+#define PGABB_LIGHT_LA 8
+#endif
+constexpr uint32_t kLightLa = PGABB_LIGHT_LA;   // |A_ix[u]| <= kLightLa (the register copy)
 constexpr uint32_t kLightLe = 32;      // |A_ij[u]| <= 32 pairs
 constexpr uint32_t kLightScan = 16;
 constexpr uint32_t kLightWork = 128;   // list loads per row
