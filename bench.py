@@ -43,6 +43,9 @@ def parse():
                     help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1)")
     ap.add_argument("--balance", choices=["measured", "cost"], default="measured",
                     help="N>1: plan pieces with measured task times (R22) or the S7 cost (R17)")
+    ap.add_argument("--budget-gb", type=float, default=0.0,
+                    help="> 0: blocks stay in pinned host memory and each count streams them through "
+                         "a device budget of this many GB (S9 out-of-core mode, PAPER.md:829-835)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
@@ -260,6 +263,9 @@ def run_ours(args):
         # S8 with rank 0's measured task times broadcast to all ranks (DESIGN R22; untimed)
         from paper_2209_04541_b200 import dist as pgd
         b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule)
+    elif args.budget_gb > 0:
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+                            residency=pg.RESIDENT_HOST, device_budget_bytes=int(args.budget_gb * (1 << 30)))
     else:
         b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
     st0 = b.stats()
@@ -339,7 +345,7 @@ def run_ours(args):
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
-    if not args.no_e2e and not vertex:
+    if not args.no_e2e and not vertex and args.budget_gb <= 0:
         bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
                              residency=pg.RESIDENT_HOST)
         for _ in range(max(1, args.warmup)):
@@ -379,6 +385,9 @@ def run_ours(args):
                        "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
                        "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}", "balance": args.balance if ws > 1 else None,
                        "comm": comm.backend,
+                       "residency": (f"host-streamed through a {args.budget_gb:g} GB device budget, "
+                                     f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B per count "
+                                     "inside the timed region") if args.budget_gb > 0 else "device",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "timer": "CUDA events per step on the launch stream, max over ranks"},
             "roofline": roofline,

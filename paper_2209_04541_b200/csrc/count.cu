@@ -465,6 +465,54 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
     return acc;
 }
 
+// Streaming residency: a warp claims the next 32 rows of the wave, one per lane;
+// each lane decodes its row (piece by binary search over the wave's piece table),
+// reads |A_ix[u]| and |A_ij[u]| and drops empty rows and light rows (k_row_flags's
+// predicate; those are k_tc_light<IMPLICIT>'s).  Returns the ballot of the heavy
+// rows (0 only when the wave is exhausted) with each lane's (task, row).
+__device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next, unsigned long long nitems,
+                                                        const WavePiece* __restrict__ wp, int nwp,
+                                                        const TaskDev* __restrict__ tasks,
+                                                        const uint32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ rowptr, int lane,
+                                                        uint32_t& t_l, uint32_t& u_l) {
+    for (;;) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(next, 32ull);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= nitems) return 0u;
+        const unsigned long long idx = b + lane;
+        bool heavy = false;
+        if (idx < nitems) {
+            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
+            }
+            t_l = wp[lo].task;
+            u_l = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
+            const TaskDev& T = tasks[t_l];
+            const uint32_t la = __ldg(rowptr + T.rp_ix + u_l + 1) - __ldg(rowptr + T.rp_ix + u_l);
+            const uint32_t e0 = __ldg(rowptr + T.rp_ij + u_l), e1 = __ldg(rowptr + T.rp_ij + u_l + 1);
+            heavy = la > 0 && e1 > e0;
+            if (heavy && la <= kLightLa && e1 - e0 <= kLightLe) {
+                bool light = T.bm_jx != ~0ull;
+                if (!light) {
+                    uint32_t work = 0;
+                    for (uint32_t e = e0; e < e1; ++e) {
+                        const uint32_t v = __ldg(col + T.col_ij + e);
+                        work += light_pair_loads(la, __ldg(rowptr + T.rp_jx + v + 1) - __ldg(rowptr + T.rp_jx + v));
+                    }
+                    light = work <= kLightWork;
+                }
+                heavy = !light;
+            }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, heavy);
+        if (m) return m;
+    }
+}
+
 // IMPLICIT = false: items[] holds the compacted row items (device-resident blocks).
 // IMPLICIT = true (streaming residency): item idx is row idx of the wave's piece
 // table wp[0..nwp) (rows of empty lists are skipped in the kernel), and the pool
@@ -491,39 +539,38 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     if (VTX)
         for (uint32_t k = lane; k < kVtxSlots / 2; k += 32) vcnt[k] = 0;   // invariant: zero between rows
     __syncwarp();
-    const unsigned long long nwarps = (unsigned long long)gridDim.x * kRowWarps;
-    // IMPLICIT: items dealt cyclically.  Otherwise warps claim kRowChunk items at a
-    // time from one counter, so the items in flight stay a narrow window of the
-    // locality-ordered list (the A_jx blocks they share stay in L2).
-    unsigned long long idx = (unsigned long long)blockIdx.x * kRowWarps + wid, claim_end = 0;
-    if (!IMPLICIT) idx = claim_items(next, nitems, lane, claim_end);
+    // Warps claim kRowChunk items at a time from one counter, so the items in
+    // flight stay a narrow window of the locality-ordered list (the A_jx blocks
+    // they share stay in L2).  IMPLICIT: item idx is row idx of the wave.
+    unsigned long long claim_end = 0;
+    unsigned long long idx = IMPLICIT ? 0 : claim_items(next, nitems, lane, claim_end);
+    uint32_t hrows = 0, t_l = 0, u_l = 0;            // IMPLICIT: heavy rows of the claimed window
 #ifdef PGABB_PROF
     unsigned long long prof[32];
     for (int c = 0; c < 32; ++c) prof[c] = 0;
     unsigned long long pt = clock64();
 #endif
-    for (; idx < nitems; idx = IMPLICIT ? idx + nwarps : (idx + 1 < claim_end ? idx + 1
-                                                                             : claim_items(next, nitems, lane, claim_end))) {
+    for (;;) {
         uint32_t t, u;
         if (IMPLICIT) {
-            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
-            }
-            t = wp[lo].task;
-            u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
+            if (!hrows && !(hrows = implicit_heavy_rows(next, nitems, wp, nwp, tasks, col, rowptr, lane, t_l, u_l)))
+                break;
+            const int bl = __ffs(hrows) - 1;
+            hrows &= hrows - 1;
+            t = __shfl_sync(0xffffffffu, t_l, bl);
+            u = __shfl_sync(0xffffffffu, u_l, bl);
         } else {
+            if (idx >= nitems) break;
             const unsigned long long it = __ldg(items + idx);
             t = (uint32_t)(it >> 32);
             u = (uint32_t)it;
+            idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
         }
         const long long c0 = TIMED ? clock64() : 0;
         const TaskDev T = tasks[t];
         const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
         const uint32_t e0 = __ldg(rowptr + T.rp_ij + u), e1 = __ldg(rowptr + T.rp_ij + u + 1);
         const uint32_t la = a1 - a0;
-        if (IMPLICIT && (la == 0 || e1 == e0)) continue;
         const uint32_t* __restrict__ A = col + T.col_ix + a0;
         const uint32_t* __restrict__ Bc = col + T.col_jx;
         const uint32_t* __restrict__ vcol = col + T.col_ij;
@@ -669,9 +716,12 @@ constexpr int kLightThreads = 256;
 #endif
 constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
 
-template <bool VTX, bool TIMED>
+// IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
+// wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
+// it is light by k_row_flags's predicate (the heavy kernel skips exactly those).
+template <bool VTX, bool TIMED, bool IMPLICIT>
 __global__ void __launch_bounds__(kLightThreads, PGABB_LIGHT_MINB)
-k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
+k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, int nwp, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
            unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
@@ -687,10 +737,38 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
     for (int r = 0; r < kLightChunk; ++r) {
         const unsigned long long idx = base + 32 * r + lane;
         if (idx >= nitems) break;
-        const uint4 it = __ldg(items + idx);
-        const uint32_t t = it.x & ((1u << kLightTaskBits) - 1), u = it.w;
-        const uint32_t la = (it.x >> kLightTaskBits) & 15u, a0 = it.y;
-        const uint32_t e0 = it.z, e1 = e0 + (it.x >> (kLightTaskBits + 4));
+        uint32_t t, u, la, a0, e0, e1;
+        if (IMPLICIT) {
+            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
+            }
+            t = wp[lo].task;
+            u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
+            const TaskDev& Tq = tasks[t];
+            a0 = __ldg(rowptr + Tq.rp_ix + u);
+            la = __ldg(rowptr + Tq.rp_ix + u + 1) - a0;
+            e0 = __ldg(rowptr + Tq.rp_ij + u);
+            e1 = __ldg(rowptr + Tq.rp_ij + u + 1);
+            if (la == 0 || e1 == e0 || la > kLightLa || e1 - e0 > kLightLe) continue;
+            if (Tq.bm_jx == ~0ull) {
+                uint32_t work = 0;
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t v = __ldg(col + Tq.col_ij + e);
+                    work += light_pair_loads(la, __ldg(rowptr + Tq.rp_jx + v + 1) - __ldg(rowptr + Tq.rp_jx + v));
+                }
+                if (work > kLightWork) continue;   // a heavy row: the warp kernel's
+            }
+        } else {
+            const uint4 it = __ldg(items + idx);
+            t = it.x & ((1u << kLightTaskBits) - 1);
+            u = it.w;
+            la = (it.x >> kLightTaskBits) & 15u;
+            a0 = it.y;
+            e0 = it.z;
+            e1 = e0 + (it.x >> (kLightTaskBits + 4));
+        }
         if (t != cur_t) {
             if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
             if (TIMED && cyc_t) atomicAdd(&cyc[cur_t], cyc_t);
@@ -906,15 +984,17 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             if (light_dev != h->device) {
                 int sms = 0, per_sm = 0;
                 PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false, false>, kLightThreads, 0));
+                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false, false, false>,
+                                                                    kLightThreads, 0));
                 light_grid = sms * std::max(per_sm, 1);
                 light_dev = h->device;
             }
             const unsigned g = (unsigned)std::max<unsigned long long>(
                 1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
-            (timed ? k_tc_light<false, true> : vtx ? k_tc_light<true, false> : k_tc_light<false, false>)
-                <<<g, kLightThreads, 0, st>>>(h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p,
-                                              h->d_bitmap.p, h->d_task_counts.p, tv, h->d_next.p,
+            (timed ? k_tc_light<false, true, false> : vtx ? k_tc_light<true, false, false>
+                                                          : k_tc_light<false, false, false>)
+                <<<g, kLightThreads, 0, st>>>(h->d_light.p, nullptr, 0, h->n_light, h->d_tasks.p, h->d_col.p,
+                                              h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p, tv, h->d_next.p,
                                               timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
@@ -940,11 +1020,23 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             PG_CK(cudaEventRecord(h->ev_copied[a], h->copy_stream));
             PG_CK(cudaStreamWaitEvent(st, h->ev_copied[a], 0));
             const uint32_t* base = h->d_arena[a].p;
+            PG_CK(cudaMemsetAsync(h->d_next.p + 2, 0, 2 * sizeof(unsigned long long), st));
             rows_kernel(true)<<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
                 nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, nullptr, nullptr);
+                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 2,
+                nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
+            {
+                const unsigned lg = (unsigned)std::max<unsigned long long>(
+                    1ull, std::min<unsigned long long>(148ull * 8, (wv.rows + kLightThreads - 1) / kLightThreads));
+                (vtx ? k_tc_light<true, false, true> : k_tc_light<false, false, true>)<<<lg, kLightThreads, 0, st>>>(
+                    nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
+                    h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv,
+                    h->d_next.p + 3, nullptr);
+                PG_LAUNCH_CHECK();
+                h->launches_last++;
+            }
             PG_CK(cudaEventRecord(h->ev_done[a], st));
         }
     }
