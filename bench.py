@@ -386,7 +386,8 @@ def run_ours(args):
                        "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}", "balance": args.balance if ws > 1 else None,
                        "comm": comm.backend,
                        "residency": (f"host-streamed through a {args.budget_gb:g} GB device budget, "
-                                     f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B per count "
+                                     f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B + D2D reuse "
+                                     f"{int(st['d2d_bytes_last'])} B per count "
                                      "inside the timed region") if args.budget_gb > 0 else "device",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "timer": "CUDA events per step on the launch stream, max over ranks"},

@@ -179,7 +179,8 @@ typedef struct {
     uint64_t max_task_bytes;            /* largest block-triple footprint (col+rowptr+dense copy) */
     uint64_t items_heavy, items_light;  /* this rank's row items: warp per row / thread per row (DESIGN R20) */
     uint64_t alg_bytes_light;           /* staged-model bytes of the light items (within alg_bytes_local) */
-    uint64_t reserved[1];
+    uint64_t d2d_bytes_last;            /* streaming: bytes re-used from the previous wave's arena
+                                           (device-to-device) by the last count call */
     double ms_build;                    /* wall time of pgabb_build_blocks */
     double ms_count_last;               /* device time of the last count call (events) */
     double ms_main_kernel_last;         /* device time of the intersection kernels (heavy + light) */

@@ -44,7 +44,7 @@ class Stats(ctypes.Structure):
                 ("cost_local", u64), ("alg_bytes_total", u64), ("alg_bytes_local", u64),
                 ("block_bytes", u64), ("h2d_bytes_last", u64), ("launches_last", u64),
                 ("waves", u64), ("max_task_bytes", u64), ("items_heavy", u64), ("items_light", u64),
-                ("alg_bytes_light", u64), ("reserved", u64 * 1), ("ms_build", ctypes.c_double),
+                ("alg_bytes_light", u64), ("d2d_bytes_last", u64), ("ms_build", ctypes.c_double),
                 ("ms_count_last", ctypes.c_double), ("ms_main_kernel_last", ctypes.c_double),
                 ("ms_light_kernel_last", ctypes.c_double), ("reserved_d", ctypes.c_double * 2)]
 

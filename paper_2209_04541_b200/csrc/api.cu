@@ -266,6 +266,7 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->items_heavy = b->n_items;
         s->items_light = b->n_light;
         s->alg_bytes_light = b->alg_light;
+        s->d2d_bytes_last = b->d2d_last;
     });
 }
 

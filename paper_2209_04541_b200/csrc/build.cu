@@ -806,11 +806,16 @@ void plan_waves(pgabb_blocks_s* h) {
     };
     struct Need { uint32_t b; int pool; };
     std::map<std::pair<uint32_t, int>, uint64_t> placed;   // (block, pool) -> arena word offset
+    // the previous wave's placement: a block it holds is copied device-to-device
+    // from the other arena instead of host-to-device (consecutive waves share blocks
+    // by the locality order: NEXT-2 block reuse)
+    std::map<std::pair<uint32_t, int>, uint64_t> prev_placed;
     Wave cur;
     std::vector<TaskDev> cur_tasks;
     auto open_wave = [&]() {
         cur = Wave{};
         cur.piece_begin = wpieces.size();
+        prev_placed.swap(placed);
         placed.clear();
         cur_tasks.assign(nt, TaskDev{});
     };
@@ -849,7 +854,9 @@ void plan_waves(pgabb_blocks_s* h) {
             const BlockInfo& B = h->blocks[key.first];
             const uint64_t src = key.second == 0 ? B.col_off : key.second == 1 ? B.rp_off : B.bm_off;
             placed[key] = cur.words;
-            if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, key.second});
+            const auto pv = prev_placed.find(key);
+            if (wd && pv != prev_placed.end()) cur.copies.push_back(StagedBlock{pv->second, cur.words, wd, 3});
+            else if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, key.second});
             cur.words += wd;
         }
         TaskDev d{};

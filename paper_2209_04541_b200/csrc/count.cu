@@ -920,6 +920,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     const int nt = (int)h->tasks.size();
     h->launches_last = 0;
     h->h2d_last = 0;
+    h->d2d_last = 0;
 
     const bool vtx = d_tv_out != nullptr;
     h->light_timed = false;
@@ -1013,6 +1014,12 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             const int a = (int)(k & 1);
             if (k >= 2) PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev_done[a], 0));
             for (const StagedBlock& c : wv.copies) {
+                if (c.pool == 3) {   // held by the previous wave: device-to-device from the other arena
+                    PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, h->d_arena[1 - a].p + c.src_word,
+                                          c.words * 4, cudaMemcpyDeviceToDevice, h->copy_stream));
+                    h->d2d_last += c.words * 4;
+                    continue;
+                }
                 PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, pools[c.pool] + c.src_word, c.words * 4,
                                       cudaMemcpyHostToDevice, h->copy_stream));
                 h->h2d_last += c.words * 4;

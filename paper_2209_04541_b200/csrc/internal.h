@@ -180,7 +180,7 @@ struct WavePiece {          // one owned piece inside a wave (device table)
 
 struct StagedBlock {        // one H2D copy: pool range -> arena offset (u32 words)
     uint64_t src_word, dst_word, words;
-    int pool;               // 0 col, 1 rowptr, 2 bitmap
+    int pool;               // 0 col, 1 rowptr, 2 bitmap (host pools); 3 = the other arena (device copy)
 };
 
 struct Wave {
@@ -247,7 +247,7 @@ struct pgabb_blocks_s {
 
     // stats
     uint64_t cost_total = 0, cost_local = 0, alg_total = 0, alg_local = 0;
-    uint64_t h2d_last = 0, launches_last = 0;
+    uint64_t h2d_last = 0, launches_last = 0, d2d_last = 0;
     double ms_build = 0, ms_count_last = 0, ms_main_last = 0, ms_light_last = 0;
     uint64_t alg_light = 0;                   // staged-model bytes of the light items
     bool light_timed = false;                 // ev_mid recorded by the last count

@@ -50,7 +50,7 @@ def test_struct_layouts():
     from paper_2209_04541_b200 import _abi
     assert ctypes.sizeof(_abi.BuildOpts) == 56
     assert ctypes.sizeof(_abi.CountOpts) == 32
-    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # 17 counters + items_heavy/light, alg_bytes_light, 1 reserved; 6 doubles
+    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # 17 counters + items_heavy/light, alg_bytes_light, d2d_bytes_last; 6 doubles
 
 
 def test_sm100a_cubin(lib_path):
