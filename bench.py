@@ -134,6 +134,7 @@ def cpu_baseline(cfg_name, n, s, d, target_s):
     """The oracle (oracle/tc_oracle.c) as it stands, on this host's cores, over a
     bounded vertex-stride sample of the same graph (full graph when it fits)."""
     import oracle
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     t0 = time.perf_counter()
     g = oracle.Graph(n, s, d)
     t_build = time.perf_counter() - t0
@@ -161,6 +162,8 @@ def run_reference(args):
         return 0
     from gen.configs import CONFIGS
     import oracle
+    # under torchrun OMP_NUM_THREADS=1: the one reference process uses every host core
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     cfg = CONFIGS[args.config]
     n, s, d = cfg.generate()
     g = oracle.Graph(n, s, d)
@@ -181,12 +184,12 @@ def run_reference(args):
     g.close()
     value = sum(edges) / sum(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "m_edges": m_edges,
-                   "sample_stride": stride},
+                   "sample_stride": stride, "device": "host CPU (the oracle; no GPU used)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
                          "sample": f"each step: node iterator over every {stride}-th vertex (rotating offset)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -62,6 +62,8 @@ def _L():
         lib.oracle_brute.restype = u64
         lib.oracle_threads.argtypes = []
         lib.oracle_threads.restype = ctypes.c_int
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_set_threads.restype = None
         _lib = lib
     return _lib
 
@@ -73,6 +75,11 @@ def _u32(a):
 
 def threads() -> int:
     return int(_L().oracle_threads())
+
+
+def set_threads(k: int) -> None:
+    """OpenMP threads of the oracle's parallel loops (all host cores by default)."""
+    _L().oracle_set_threads(int(k))
 
 
 class Graph:

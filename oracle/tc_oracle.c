@@ -245,3 +245,5 @@ uint64_t oracle_brute(uint32_t n, uint64_t m, const uint32_t* src, const uint32_
 }
 
 int oracle_threads(void) { return omp_get_max_threads(); }
+/* thread count for later parallel regions (torchrun sets OMP_NUM_THREADS=1 per rank) */
+void oracle_set_threads(int k) { if (k > 0) omp_set_num_threads(k); }
