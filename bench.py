@@ -39,8 +39,9 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
     ap.add_argument("--cut-rule", type=int, default=0)
-    ap.add_argument("--path", choices=["count", "vertex"], default="count",
-                    help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1)")
+    ap.add_argument("--path", choices=["count", "vertex", "cc"], default="count",
+                    help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1); "
+                         "cc: Shiloach-Vishkin connected components on the same blocks (NEXT-4)")
     ap.add_argument("--balance", choices=["measured", "cost"], default="measured",
                     help="N>1: plan pieces with measured task times (R22) or the S7 cost (R17)")
     ap.add_argument("--budget-gb", type=float, default=0.0,
@@ -413,10 +414,81 @@ def run_ours(args):
     return 0
 
 
+def run_cc(args):
+    """NEXT-4: SV connected components on the TC blocks, one GPU.
+    value = |E| / device time of one whole HOOK/LINK loop (CUDA events inside the call)."""
+    import torch
+
+    from gen.configs import CONFIGS
+    import oracle
+    import paper_2209_04541_b200 as pg
+    ws, rank, local = dist_env()
+    if ws > 1:
+        if rank == 0:
+            print(json.dumps({"metric": "connected-components edges/sec (|E|/time)", "unavailable":
+                              "connected components run on one GPU (world_size 1)"}), flush=True)
+        return 0
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[args.config]
+    p = args.p or cfg.p
+    n, s, d = cfg.generate()
+    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=0)
+    st0 = b.stats()
+    m_edges = int(st0["m_edges"])
+    lab = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        _, ncomp, iters = b.connected_components(out=lab)
+    ms = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            _, ncomp, iters = b.connected_components(out=lab)
+            ms.append(b.stats()["ms_cc_last"])
+    ms_step = statistics.mean(ms)
+    peak, peak_src = load_peaks()
+    # per SV round: the hook pass reads every col id (4 B) and C of both ends (8 B) per
+    # edge plus one rowptr pair per row; the link pass reads and writes C (8 B per vertex)
+    alg = iters * (12 * m_edges + 8 * n) + 4 * n
+    ach = alg / (ms_step / 1e3) / 1e9
+    line = {"metric": "connected-components edges/sec (|E|/time)", "value": m_edges / (ms_step / 1e3),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "path": "cc", "n": n, "m_edges": m_edges,
+                       "p": int(st0["p"]), "components": ncomp, "sv_rounds": iters,
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "timer": "CUDA events inside pgabb_connected_components (HOOK/LINK loop + labels)"},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None, "kernel": "k_cc_hook + k_cc_link (all SV rounds)",
+                         "alg_bytes_per_launch": alg, "peak_source": peak_src,
+                         "model": "per round 12 B/edge + 8 B/vertex (+4 B/vertex labels)"},
+            "clocks": clk.summary(), "gpu_launches": 2 * iters + 3}
+    if not args.no_cpu:
+        import time as _t
+        oracle.set_threads(len(os.sched_getaffinity(0)))
+        g = oracle.Graph(n, s, d)
+        t0 = _t.perf_counter()
+        want, k = g.components()
+        dt = _t.perf_counter() - t0
+        g.close()
+        import numpy as np
+        got = lab[:n].cpu().numpy().astype(np.uint32)
+        line["cpu_baseline"] = {"value": m_edges / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": "full graph: sequential union-find (oracle_components)"}
+        line["parity"] = {"oracle_components": k, "match": bool(k == ncomp and np.array_equal(got, want))}
+    b.free()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.path == "cc":
+        return run_cc(args)
     return run_ours(args)
 
 

@@ -185,7 +185,8 @@ typedef struct {
     double ms_count_last;               /* device time of the last count call (events) */
     double ms_main_kernel_last;         /* device time of the intersection kernels (heavy + light) */
     double ms_light_kernel_last;        /* device time of the light-row kernel alone */
-    double reserved_d[2];
+    double ms_cc_last;                  /* device time of the last pgabb_connected_components */
+    double reserved_d[1];
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);
@@ -202,6 +203,20 @@ PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats)
  * Errors: EINVAL (NULL argument), ECUDA.
  */
 PGABB_API pgabb_status_t pgabb_task_times(pgabb_blocks_t b, uint64_t* ns);
+
+/*
+ * Connected components: Shiloach-Vishkin on the same blocks
+ * (Listing 2): HOOK (for every edge, hook the greater root under
+ * the smaller) and LINK (pointer jumping) alternate until a HOOK pass hooks nothing.
+ *   labels: uint32[n], ORIGINAL ids: labels[v] = the smallest original id in v's
+ *           component (a canonical labelling: isolated ids label themselves).
+ *           HOST, or DEVICE with opts->flags & PGABB_OUT_DEVICE.
+ *   ncomponents, iterations: optional outputs (HOOK+LINK rounds, the last one hooks 0).
+ * One GPU (world_size 1), blocks resident or host-resident without a budget
+ * (EINVAL otherwise).  Synchronous.  Errors: EINVAL, ENOMEM, ECUDA.
+ */
+PGABB_API pgabb_status_t pgabb_connected_components(pgabb_blocks_t b, const pgabb_count_opts_t* opts,
+                                          uint32_t* labels, uint64_t* ncomponents, uint32_t* iterations);
 
 /* ---- introspection (parity tests of S2..S8); all outputs are HOST buffers ---- */
 

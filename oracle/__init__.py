@@ -62,6 +62,8 @@ def _L():
         lib.oracle_brute.restype = u64
         lib.oracle_threads.argtypes = []
         lib.oracle_threads.restype = ctypes.c_int
+        lib.oracle_components.argtypes = [vp, u32p]
+        lib.oracle_components.restype = u64
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         lib.oracle_set_threads.restype = None
         _lib = lib
@@ -133,6 +135,14 @@ class Graph:
         T = int(_L().oracle_count_range(self._h, v0, v1, stride, None, ctypes.byref(e)))
         return T, int(e.value)
 
+    def components(self):
+        """(labels, ncomponents): labels[v] = smallest id of v's component in G_s."""
+        lab = np.zeros(max(self.n, 1), np.uint32)
+        nc = int(_L().oracle_components(self._h, lab.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+        if nc == (1 << 64) - 1:
+            raise MemoryError("oracle union-find array")
+        return lab[:self.n], nc
+
     def wedges(self) -> int:
         """W = sum_v d-(v) d+(v) over the degree-ordered DAG."""
         return int(_L().oracle_wedges(self._h))
@@ -141,6 +151,13 @@ class Graph:
 def count(n, src, dst, per_vertex: bool = False):
     with Graph(n, src, dst) as g:
         return g.count(per_vertex)
+
+
+def components(n, src, dst):
+    """Connected components (NEXT-4): (labels, ncomponents), labels[v] = smallest id
+    in v's component (union-find, tc_oracle.c)."""
+    with Graph(n, src, dst) as g:
+        return g.components()
 
 
 def clustering(n, src, dst):

@@ -247,3 +247,39 @@ uint64_t oracle_brute(uint32_t n, uint64_t m, const uint32_t* src, const uint32_
 int oracle_threads(void) { return omp_get_max_threads(); }
 /* thread count for later parallel regions (torchrun sets OMP_NUM_THREADS=1 per rank) */
 void oracle_set_threads(int k) { if (k > 0) omp_set_num_threads(k); }
+
+/*
+ * Connected components of G_s (the problem the paper's
+ * Shiloach-Vishkin example solves): labels[v] = the smallest
+ * vertex id of v's component.  Plain sequential union-find over the undirected
+ * adjacency: the root of every tree is the smallest id in it (a union hangs the
+ * greater root under the smaller one), find() halves paths.  Returns the number
+ * of components.  Pinned by tests/test_oracle.py (scipy connected_components,
+ * BFS on small graphs, closed forms).
+ */
+static uint32_t uf_find(uint32_t* par, uint32_t x) {
+    while (par[x] != x) {
+        par[x] = par[par[x]];
+        x = par[x];
+    }
+    return x;
+}
+
+uint64_t oracle_components(const oracle_graph* g, uint32_t* labels) {
+    const uint32_t n = g->n;
+    uint32_t* par = (uint32_t*)malloc((size_t)(n ? n : 1) * 4);
+    if (!par) return ~0ull;
+    for (uint32_t v = 0; v < n; ++v) par[v] = v;
+    for (uint32_t v = 0; v < n; ++v)
+        for (uint64_t k = g->beg[v]; k < g->beg[v] + g->deg[v]; ++k) {
+            const uint32_t a = uf_find(par, v), b = uf_find(par, g->adj[k]);
+            if (a != b) par[a > b ? a : b] = a < b ? a : b;
+        }
+    uint64_t nc = 0;
+    for (uint32_t v = 0; v < n; ++v) {
+        labels[v] = uf_find(par, v);
+        nc += (labels[v] == v);
+    }
+    free(par);
+    return nc;
+}

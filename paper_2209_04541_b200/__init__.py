@@ -150,6 +150,26 @@ class Blocks:
             "pgabb_local_clustering")
         return cc[:self.n]
 
+    def connected_components(self, stream=None, out=None):
+        """Shiloach-Vishkin components (NEXT-4): (labels, ncomponents, iterations);
+        labels[v] = smallest original id of v's component (numpy uint32[n], or
+        written into ``out``, a CUDA 4-byte tensor of n entries)."""
+        o = _abi.CountOpts()
+        if stream is not None:
+            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+        nc, it = ctypes.c_uint64(0), ctypes.c_uint32(0)
+        if out is not None:
+            if not getattr(out, "is_cuda", False) or out.numel() < self.n or out.element_size() != 4:
+                raise ValueError("out must be a CUDA 4-byte tensor with >= n entries")
+            o.flags = _abi.OUT_DEVICE
+            _ck(_lib.pgabb_connected_components(self._h, ctypes.byref(o), out.data_ptr(), ctypes.byref(nc),
+                                                ctypes.byref(it)), "pgabb_connected_components")
+            return out[:self.n], int(nc.value), int(it.value)
+        lab = np.zeros(max(self.n, 1), np.uint32)
+        _ck(_lib.pgabb_connected_components(self._h, ctypes.byref(o), lab.ctypes.data, ctypes.byref(nc),
+                                            ctypes.byref(it)), "pgabb_connected_components")
+        return lab[:self.n], int(nc.value), int(it.value)
+
     def task_times(self) -> np.ndarray:
         """Measured device time per task (ns, uint64[ntasks]) of this handle's pieces:
         the scheduler's E(t) for a balanced multi-GPU plan (pgabb_task_times)."""

@@ -46,7 +46,8 @@ class Stats(ctypes.Structure):
                 ("waves", u64), ("max_task_bytes", u64), ("items_heavy", u64), ("items_light", u64),
                 ("alg_bytes_light", u64), ("d2d_bytes_last", u64), ("ms_build", ctypes.c_double),
                 ("ms_count_last", ctypes.c_double), ("ms_main_kernel_last", ctypes.c_double),
-                ("ms_light_kernel_last", ctypes.c_double), ("reserved_d", ctypes.c_double * 2)]
+                ("ms_light_kernel_last", ctypes.c_double), ("ms_cc_last", ctypes.c_double),
+                ("reserved_d", ctypes.c_double * 1)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}
@@ -61,6 +62,7 @@ SIGNATURES = [
     ("pgabb_local_clustering", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, vp]),
     ("pgabb_get_stats", ctypes.c_int, [vp, ctypes.POINTER(Stats)]),
     ("pgabb_task_times", ctypes.c_int, [vp, u64p]),
+    ("pgabb_connected_components", ctypes.c_int, [vp, ctypes.POINTER(CountOpts), vp, u64p, u32p]),
     ("pgabb_get_rank", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_cuts", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_block", ctypes.c_int, [vp, u32, u32, u32p, u32p, u64p]),

@@ -234,6 +234,16 @@ pgabb_status_t pgabb_task_times(pgabb_blocks_t b, uint64_t* ns) {
     });
 }
 
+pgabb_status_t pgabb_connected_components(pgabb_blocks_t b, const pgabb_count_opts_t* opts, uint32_t* labels,
+                                         uint64_t* ncomponents, uint32_t* iterations) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "handle is NULL");
+        if (!labels && b->n) fail(PGABB_EINVAL, "labels is NULL");
+        DeviceGuard g(b->device);
+        connected_components(b, opts, labels, ncomponents, iterations);
+    });
+}
+
 pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
     return guarded([&] {
         if (!b || !s) fail(PGABB_EINVAL, "NULL argument");
@@ -263,6 +273,7 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->ms_count_last = b->ms_count_last;
         s->ms_main_kernel_last = b->ms_main_last;
         s->ms_light_kernel_last = b->ms_light_last;
+        s->ms_cc_last = b->ms_cc_last;
         s->items_heavy = b->n_items;
         s->items_light = b->n_light;
         s->alg_bytes_light = b->alg_light;

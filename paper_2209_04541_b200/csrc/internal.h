@@ -249,6 +249,8 @@ struct pgabb_blocks_s {
     uint64_t cost_total = 0, cost_local = 0, alg_total = 0, alg_local = 0;
     uint64_t h2d_last = 0, launches_last = 0, d2d_last = 0;
     double ms_build = 0, ms_count_last = 0, ms_main_last = 0, ms_light_last = 0;
+    double ms_cc_last = 0;                    // device time of the last connected-components call
+    uint32_t cc_iters_last = 0;
     uint64_t alg_light = 0;                   // staged-model bytes of the light items
     bool light_timed = false;                 // ev_mid recorded by the last count
     bool timing_pending = false;   // events of the last (async) count not read yet
@@ -264,6 +266,8 @@ void plan_waves(pgabb_blocks_s* h);
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
                          unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr);
 void task_times(pgabb_blocks_s* h, uint64_t* ns);
+void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uint32_t* labels, uint64_t* ncomp,
+                          uint32_t* iters);
 void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc);
 void resolve_timing(pgabb_blocks_s* h);
 }  // namespace pgabb

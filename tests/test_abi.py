@@ -50,7 +50,7 @@ def test_struct_layouts():
     from paper_2209_04541_b200 import _abi
     assert ctypes.sizeof(_abi.BuildOpts) == 56
     assert ctypes.sizeof(_abi.CountOpts) == 32
-    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # 17 counters + items_heavy/light, alg_bytes_light, d2d_bytes_last; 6 doubles
+    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # + ms_cc_last took a reserved double   # 17 counters + items_heavy/light, alg_bytes_light, d2d_bytes_last; 6 doubles
 
 
 def test_sm100a_cubin(lib_path):
@@ -77,5 +77,6 @@ def test_null_arguments_rejected():
     assert lib.pgabb_triangle_count(None, None, None) == 1
     assert lib.pgabb_vertex_triangles(None, None, None, None) == 1
     assert lib.pgabb_local_clustering(None, None, None, None) == 1
+    assert lib.pgabb_connected_components(None, None, None, None, None) == 1
     lib.pgabb_free(None)   # no-op
     assert pg.version().startswith("pgabb")

@@ -233,3 +233,51 @@ def test_clustering_closed_forms():
     e = np.zeros(0, np.uint32)
     tv, cc = oracle.clustering(5, e, e)               # isolated vertices: deg < 2 -> 0
     assert (tv == 0).all() and (cc == 0.0).all()
+
+
+# ---- connected components (NEXT-4) --------------------------
+def _bfs_components(n, s, d):
+    adj = [[] for _ in range(n)]
+    for a, b in zip(s, d):
+        if a != b:
+            adj[int(a)].append(int(b))
+            adj[int(b)].append(int(a))
+    lab = [-1] * n
+    for v in range(n):           # ascending v: the first vertex reached is the smallest id
+        if lab[v] >= 0:
+            continue
+        lab[v] = v
+        stack = [v]
+        while stack:
+            x = stack.pop()
+            for y in adj[x]:
+                if lab[y] < 0:
+                    lab[y] = v
+                    stack.append(y)
+    return lab
+
+
+def test_components_vs_bfs_and_scipy():
+    from scipy.sparse.csgraph import connected_components
+    for n, s, d in (gen.er_small(300, 0.004, seed=1), gen.rmat(9, 2, seed=2),
+                    gen.disjoint_union(gen.path(30), gen.complete(5), gen.star(9), gen.cycle(7))):
+        lab, nc = oracle.components(n, s, d)
+        assert [int(x) for x in lab] == _bfs_components(n, s, d)
+        A = sp.coo_matrix((np.ones(s.size), (s, d)), shape=(n, n))
+        k, sl = connected_components(A, directed=False)
+        assert nc == k
+        # same partition: labels and scipy's component ids are in bijection
+        assert len(set(zip(lab.tolist(), sl.tolist()))) == k
+
+
+def test_components_closed_forms():
+    lab, nc = oracle.components(*gen.path(100))
+    assert nc == 1 and (lab == 0).all()
+    g = gen.clique_union([3, 9, 1, 64])          # 4 cliques, one a single vertex
+    lab, nc = oracle.components(*g)
+    assert nc == 4 and sorted(set(lab.tolist())) == [0, 3, 12, 13]
+    e = np.zeros(0, np.uint32)
+    lab, nc = oracle.components(6, e, e)          # isolated ids label themselves
+    assert nc == 6 and lab.tolist() == list(range(6))
+    lab, nc = oracle.components(*gen.messy(gen.cycle(50), seed=3))   # noise does not change G_s
+    assert nc == 1
