@@ -9,6 +9,7 @@ c2 is also re-counted by the oracle in the test itself.
 import json
 import os
 
+import numpy as np
 import pytest
 
 import gen
@@ -75,3 +76,27 @@ def test_c5_streamed_out_of_core():
     _, T, st = run("c5", residency=pg.RESIDENT_HOST, device_budget_bytes=6 << 30)
     assert st["waves"] > 1
     assert T == GOLDEN["c5"]["triangles"]
+
+
+def test_c2_per_vertex_and_clustering_full():
+    # NEXT-1 at the bench's c2 size: every t(v) and cc(v) against the oracle
+    cfg = CONFIGS["c2"]
+    n, s, d = cfg.generate()
+    want_tv, want_cc = oracle.clustering(n, s, d)
+    with pg.build_blocks(n, s, d, p=cfg.p) as b:
+        tv, T = b.vertex_triangles()
+        cc = b.local_clustering(tv)
+    assert T == GOLDEN["c2"]["triangles"]
+    assert np.array_equal(tv, want_tv)
+    assert np.array_equal(cc, want_cc)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_components_full(name):
+    # NEXT-4 at full size: every label against the oracle's union-find
+    cfg = CONFIGS[name]
+    n, s, d = cfg.generate()
+    want, k = oracle.components(n, s, d)
+    with pg.build_blocks(n, s, d, p=cfg.p) as b:
+        lab, kk, _ = b.connected_components()
+    assert kk == k and np.array_equal(lab, want)
