@@ -545,6 +545,8 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     unsigned long long claim_end = 0;
     unsigned long long idx = IMPLICIT ? 0 : claim_items(next, nitems, lane, claim_end);
     uint32_t hrows = 0, t_l = 0, u_l = 0;            // IMPLICIT: heavy rows of the claimed window
+    uint32_t cur_t = 0;                              // task of the warp's running count
+    unsigned long long acc_t = 0;
 #ifdef PGABB_PROF
     unsigned long long prof[32];
     for (int c = 0; c < 32; ++c) prof[c] = 0;
@@ -576,8 +578,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         const uint32_t* __restrict__ vcol = col + T.col_ij;
         const uint32_t* __restrict__ rp_jx = rowptr + T.rp_jx;
         const int mode = (T.wx <= kWarpBitmapBits) ? 0 : (la <= kHashMaxList ? 1 : 2);
-        uint32_t hbits = 5;
-        while ((1u << hbits) < 2 * la) ++hbits;
+        const uint32_t hbits = max(5, 32 - __clz(2 * la - 1));   // smallest 2^hbits >= 2 la (>= 32)
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
         unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
@@ -674,13 +675,19 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         __syncwarp();
         // a row's count is < 2^32 (<= |A_ix[u]| * |A_ij[u]|), so a 32-bit REDUX suffices
         const uint32_t sum = __reduce_add_sync(0xffffffffu, acc);
-        if (lane == 0 && sum) {
-            atomicAdd(&task_counts[t], (unsigned long long)sum);
-            if (VTX) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
+        // the warp keeps its count while consecutive items share a task (one atomic per
+        // task change instead of one per row: the rows of a task all add to one counter)
+        if (t != cur_t) {
+            if (lane == 0 && acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+            cur_t = t;
+            acc_t = 0;
         }
+        acc_t += sum;
+        if (VTX && lane == 0 && sum) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
         if (TIMED && lane == 0) atomicAdd(&cyc[t], (unsigned long long)(clock64() - c0));
         PROF_MARK(7);
     }
+    if (lane == 0 && acc_t) atomicAdd(&task_counts[cur_t], acc_t);
 #ifdef PGABB_PROF
     if (lane == 0)
         for (int c = 0; c < 32; ++c)
