@@ -88,6 +88,13 @@ constexpr int kAndUnroll = PGABB_AND_UNROLL;   // v rows in flight per lane grou
 #define PGABB_DENSE_UNROLL 4
 #endif
 constexpr int kDenseUnroll = PGABB_DENSE_UNROLL;   // bit tests in flight per lane in probe_dense_row
+// probe_dense_row (one scattered bit test per element of A_ix[u] per pair) instead
+// of staging + the AND path (W coalesced words, W/8 sectors per pair) when
+// |A_ix[u]| <= kDenseRowMul * W / 8
+#ifndef PGABB_DENSE_ROW_MUL
+#define PGABB_DENSE_ROW_MUL 16
+#endif
+constexpr uint32_t kDenseRowMul = PGABB_DENSE_ROW_MUL;
 #ifndef PGABB_ROW_CHUNK
 #define PGABB_ROW_CHUNK 4
 #endif
@@ -585,7 +592,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
         VCnt vc{vcnt, vpre, tvx, false};
         PROF_MARK(0);
-        if (T.bm_jx != ~0ull && la <= 2 * T.bm_words) {
+        if (T.bm_jx != ~0ull && 8 * la <= kDenseRowMul * T.bm_words) {
             acc = probe_dense_row<VTX>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);

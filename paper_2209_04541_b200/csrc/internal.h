@@ -153,9 +153,18 @@ constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
 #define PGABB_LIGHT_LA 8
 #endif
 constexpr uint32_t kLightLa = PGABB_LIGHT_LA;   // |A_ix[u]| <= kLightLa (the register copy)
-constexpr uint32_t kLightLe = 32;      // |A_ij[u]| <= 32 pairs
-constexpr uint32_t kLightScan = 16;
-constexpr uint32_t kLightWork = 128;   // list loads per row
+#ifndef PGABB_LIGHT_LE
+#define PGABB_LIGHT_LE 32
+#endif
+constexpr uint32_t kLightLe = PGABB_LIGHT_LE;      // |A_ij[u]| <= 32 pairs
+#ifndef PGABB_LIGHT_SCAN
+#define PGABB_LIGHT_SCAN 16
+#endif
+constexpr uint32_t kLightScan = PGABB_LIGHT_SCAN;
+#ifndef PGABB_LIGHT_WORK
+#define PGABB_LIGHT_WORK 128
+#endif
+constexpr uint32_t kLightWork = PGABB_LIGHT_WORK;   // list loads per row
 // A light item carries its row's offsets, so the kernel starts with the lists
 // instead of a chain of descriptor / rowptr loads:
 //   x = task | |A_ix[u]| << 16 | |A_ij[u]| << 20,  y = rowptr_ix[u],  z = rowptr_ij[u],  w = u
