@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
     ap.add_argument("--cut-rule", type=int, default=0)
-    ap.add_argument("--path", choices=["count", "vertex", "cc"], default="count",
+    ap.add_argument("--path", choices=["count", "vertex", "vertex2", "cc"], default="count",
+                    # vertex2: the two-pass route of R24 (measured far slower: kept for the record)
                     help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1); "
                          "cc: Shiloach-Vishkin connected components on the same blocks (NEXT-4)")
     ap.add_argument("--balance", choices=["measured", "cost"], default="measured",
@@ -280,10 +281,20 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-    vertex = args.path == "vertex"
+    vertex = args.path in ("vertex", "vertex2")
     tv_dev = torch.zeros(max(n, 1), dtype=torch.int64, device="cuda") if vertex else None
+    b_rev = None
+    if args.path == "vertex2":   # the reversed-order handle of the two-pass route (R24)
+        b_rev = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+                                reverse_order=True)
 
     def step():
+        if b_rev is not None:
+            # t(v): lowest+middle roles on the forward handle, + lowest on the reversed one
+            b.vertex_triangles(stream=stream, out=tv_dev, sync=False, roles="low+mid")
+            b_rev.vertex_triangles(stream=stream, out=tv_dev, sync=False, roles="low", accumulate=True)
+            comm.allreduce_(tv_dev)
+            return
         if vertex:
             # per-vertex t(v) on the device, then one allreduce of the n-vector
             b.vertex_triangles(stream=stream, out=tv_dev, sync=False)
@@ -312,6 +323,11 @@ def run_ours(args):
             kern_ms.append(stk["ms_main_kernel_last"])
             light_ms.append(stk["ms_light_kernel_last"])
             launches += int(stk["launches_last"])
+            if b_rev is not None:   # the second pass's kernels count toward the step too
+                sr = b_rev.stats()
+                kern_ms[-1] += sr["ms_main_kernel_last"]
+                light_ms[-1] += sr["ms_light_kernel_last"]
+                launches += int(sr["launches_last"])
         torch.cuda.synchronize()
         comm.barrier()
     step_ms = [a.elapsed_time(z) for a, z in ev]
@@ -327,9 +343,11 @@ def run_ours(args):
     if vertex:
         # + the t(v) vector: zeroed and read once in rank space, written once in original ids
         alg += 3 * 8 * n
+    if b_rev is not None:   # the reversed pass streams its own staged-model bytes
+        alg += int(b_rev.stats()["alg_bytes_local"]) + 3 * 8 * n
     kms = statistics.mean(kern_ms) if kern_ms else float("nan")
     lms = statistics.mean(light_ms) if light_ms else 0.0
-    alg_l = int(st["alg_bytes_light"])
+    alg_l = int(st["alg_bytes_light"]) + (int(b_rev.stats()["alg_bytes_light"]) if b_rev is not None else 0)
 
     def kern(name, ms, nbytes):
         ach = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
@@ -381,6 +399,8 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC if not vertex else "per-vertex triangle-count edges/sec (|E|/time)",
+            "vertex_route": ("two-pass (low+mid forward, low reversed; R24)" if b_rev is not None
+                             else "one-pass (all roles)") if vertex else None,
             "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -410,6 +430,8 @@ def run_ours(args):
                               "source": "tests/golden/triangles.json (oracle-only script)"}
         print(json.dumps(line), flush=True)
     b.free()
+    if b_rev is not None:
+        b_rev.free()
     comm.close()
     return 0
 

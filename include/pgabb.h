@@ -79,7 +79,11 @@ typedef struct {
     int32_t rank;               /* this handle's rank in [0, world_size) (S8) */
     int32_t world_size;         /* ranks sharing the tasks; <= 1 means one GPU */
     uint32_t residency;         /* PGABB_RESIDENT_DEVICE or PGABB_RESIDENT_HOST */
-    uint32_t reserved0;
+    uint32_t reverse_order;     /* 1: S2 ranks are reversed (rank = n-1-position in the
+                                   (deg, id) order), so the DAG runs from high degree to
+                                   low; triangle counts are unchanged, and each triangle's
+                                   lowest and highest vertices swap roles (NEXT-1 two-pass
+                                   per-vertex counts, DESIGN R24) */
     uint64_t device_budget_bytes; /* HOST residency: device bytes for staged blocks;
                                      0 = stage all of this rank's blocks at once */
     const uint64_t* task_weights; /* optional HOST uint64[n_task_weights]: the task
@@ -121,7 +125,15 @@ typedef struct {
 } pgabb_count_opts_t;
 
 #define PGABB_COUNT_ASYNC 1u
-#define PGABB_OUT_DEVICE 2u     /* pgabb_vertex_triangles / pgabb_local_clustering: the
+#define PGABB_OUT_DEVICE 2u
+/* pgabb_vertex_triangles roles (DESIGN R24): which vertices of a triangle {u<v<w}
+   (rank order) are credited.  None set = all three.  Allowed: LOW, LOW|MID, LOW|MID|HIGH. */
+#define PGABB_ROLE_LOW 4u
+#define PGABB_ROLE_MID 8u
+#define PGABB_ROLE_HIGH 16u
+/* pgabb_vertex_triangles with PGABB_OUT_DEVICE: ADD this pass's t(v) into tv instead
+   of overwriting it (the second pass of the two-pass route) */
+#define PGABB_OUT_ACCUMULATE 32u     /* pgabb_vertex_triangles / pgabb_local_clustering: the
                                    tv and cc arrays are DEVICE pointers on the handle's
                                    device (stream-ordered on opts->cuda_stream) */
 
@@ -137,7 +149,12 @@ PGABB_API pgabb_status_t pgabb_triangle_count(pgabb_blocks_t b, const pgabb_coun
                                     uint64_t* triangles);
 
 /*
- * Per-vertex triangle counts.  The paper motivates
+ * Per-vertex triangle counts.  opts->flags may restrict the
+ * credited roles (PGABB_ROLE_*): LOW credits only each triangle's lowest-rank vertex
+ * (one row total per (task,row): no per-hit atomics), LOW|MID adds the middle vertex
+ * (per pair).  A handle built with reverse_order swaps LOW and HIGH, so
+ *   t = [LOW|MID on the forward handle] + [LOW on the reversed handle]
+ * is the cheap two-pass route to t(v); LOW|MID|HIGH on one handle is the one-pass route.  The paper motivates
  * triangle counting as the way "to measure clustering coefficients"
  * (§1); t(v) is the number of triangles containing v.
  * Same S9-S11 path as pgabb_triangle_count; every triangle {u<v<w} (rank

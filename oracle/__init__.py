@@ -62,6 +62,8 @@ def _L():
         lib.oracle_brute.restype = u64
         lib.oracle_threads.argtypes = []
         lib.oracle_threads.restype = ctypes.c_int
+        lib.oracle_count_roles.argtypes = [vp, u64p, u64p, u64p]
+        lib.oracle_count_roles.restype = u64
         lib.oracle_components.argtypes = [vp, u32p]
         lib.oracle_components.restype = u64
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
@@ -135,6 +137,16 @@ class Graph:
         T = int(_L().oracle_count_range(self._h, v0, v1, stride, None, ctypes.byref(e)))
         return T, int(e.value)
 
+    def count_roles(self):
+        """(T, tlow, tmid, thigh): per-vertex counts of the triangles in which the
+        vertex is the lowest / middle / highest in the (deg, id) order (R24)."""
+        arrs = [np.zeros(max(self.n, 1), np.uint64) for _ in range(3)]
+        ptr = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) for a in arrs]
+        T = int(_L().oracle_count_roles(self._h, *ptr))
+        if T == (1 << 64) - 1:
+            raise MemoryError("oracle mark array")
+        return (T, *[a[:self.n] for a in arrs])
+
     def components(self):
         """(labels, ncomponents): labels[v] = smallest id of v's component in G_s."""
         lab = np.zeros(max(self.n, 1), np.uint32)
@@ -151,6 +163,12 @@ class Graph:
 def count(n, src, dst, per_vertex: bool = False):
     with Graph(n, src, dst) as g:
         return g.count(per_vertex)
+
+
+def count_roles(n, src, dst):
+    """(T, tlow, tmid, thigh) by role in the degree order (DESIGN R24)."""
+    with Graph(n, src, dst) as g:
+        return g.count_roles()
 
 
 def components(n, src, dst):

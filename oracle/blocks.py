@@ -31,12 +31,13 @@ def degrees(n: int, E: np.ndarray) -> np.ndarray:
     return np.bincount(E.ravel(), minlength=n).astype(np.int64)
 
 
-def degree_rank(n: int, deg: np.ndarray) -> np.ndarray:
-    """rank[v] = position of v when vertices are sorted by (deg, id) ascending."""
+def degree_rank(n: int, deg: np.ndarray, reverse: bool = False) -> np.ndarray:
+    """rank[v] = position of v when vertices are sorted by (deg, id) ascending;
+    reverse (reading R24): n - 1 - that position."""
     order = np.lexsort((np.arange(n), deg))
     rank = np.empty(n, np.int64)
     rank[order] = np.arange(n)
-    return rank
+    return (n - 1 - rank) if reverse else rank
 
 
 # S3 -- orient + relabel (PAPER.md:1410-1411 "only requires half of the edges";
@@ -246,11 +247,11 @@ def piece_count(B, t, r0: int, r1: int) -> int:
 class Plan:
     """All intermediate objects of the block method for one (graph, p, rule, G)."""
 
-    def __init__(self, n, src, dst, p, rule=0, G=1, weights=None):
+    def __init__(self, n, src, dst, p, rule=0, G=1, weights=None, reverse=False):
         self.n = int(n)
         self.E = canonical_edges(n, src, dst)
         self.deg = degrees(n, self.E)
-        self.rank = degree_rank(n, self.deg)
+        self.rank = degree_rank(n, self.deg, reverse)
         self.D = dag(self.E, self.rank)
         self.p = effective_p(n, p)
         self.cuts = cuts(n, self.D, self.p, rule)

@@ -283,3 +283,37 @@ uint64_t oracle_components(const oracle_graph* g, uint32_t* labels) {
     free(par);
     return nc;
 }
+
+/*
+ * Per-vertex counts split by role (DESIGN R24): for every triangle v < u < w in
+ * the degree order, tlow[v], tmid[u], thigh[w] += 1.  The node iterator of
+ * oracle_count_range, sequential, with three arrays.  tlow + tmid + thigh = t.
+ */
+uint64_t oracle_count_roles(const oracle_graph* g, uint64_t* tlow, uint64_t* tmid, uint64_t* thigh) {
+    const uint64_t words = ((uint64_t)g->n + 63) / 64;
+    uint64_t* mark = (uint64_t*)calloc(words ? words : 1, sizeof(uint64_t));
+    if (!mark) return ~0ull;
+    uint64_t T = 0;
+    for (uint32_t v = 0; v < g->n; ++v) {
+        const uint32_t* Nv = g->padj + g->pbeg[v];
+        const uint64_t dv = g->pbeg[v + 1] - g->pbeg[v];
+        for (uint64_t i = 0; i < dv; ++i) mark[Nv[i] >> 6] |= 1ull << (Nv[i] & 63);
+        for (uint64_t i = 0; i < dv; ++i) {
+            const uint32_t u = Nv[i];
+            const uint32_t* Nu = g->padj + g->pbeg[u];
+            const uint64_t du = g->pbeg[u + 1] - g->pbeg[u];
+            for (uint64_t k = 0; k < du; ++k) {
+                const uint32_t w = Nu[k];
+                if (mark[w >> 6] >> (w & 63) & 1ull) {
+                    ++T;
+                    tlow[v]++;
+                    tmid[u]++;
+                    thigh[w]++;
+                }
+            }
+        }
+        for (uint64_t i = 0; i < dv; ++i) mark[Nv[i] >> 6] = 0;
+    }
+    free(mark);
+    return T;
+}

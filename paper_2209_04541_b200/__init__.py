@@ -106,18 +106,22 @@ class Blocks:
         return (int(out.value), tc[:self.ntasks]) if task_counts else int(out.value)
 
     # --- per-vertex counts ---
-    def vertex_triangles(self, stream=None, out=None, sync: bool = True):
+    def vertex_triangles(self, stream=None, out=None, sync: bool = True, roles: str = "all",
+                         accumulate: bool = False):
         """This rank's t(v) for every original id v (numpy uint64[n]), or, with
         ``out`` a CUDA int64/uint64 tensor of n entries, written into it on the
-        device (stream-ordered; ready for an NCCL allreduce).  Returns (tv, T_rank)."""
+        device (stream-ordered; ready for an NCCL allreduce).  Returns (tv, T_rank).
+        roles: "all", "low" or "low+mid" -- which vertices of each triangle
+        {u<v<w} (rank order) are credited (DESIGN R24)."""
         o = _abi.CountOpts()
+        o.flags = {"all": 0, "low": _abi.ROLE_LOW, "low+mid": _abi.ROLE_LOW | _abi.ROLE_MID}[roles]
         if stream is not None:
             o.cuda_stream = getattr(stream, "cuda_stream", stream)
         cnt = ctypes.c_uint64(0)
         if out is not None:
             if not getattr(out, "is_cuda", False) or out.numel() < self.n or out.element_size() != 8:
                 raise ValueError("out must be a CUDA 8-byte tensor with >= n entries")
-            o.flags = _abi.OUT_DEVICE | (0 if sync else _abi.COUNT_ASYNC)
+            o.flags |= _abi.OUT_DEVICE | (0 if sync else _abi.COUNT_ASYNC) | (_abi.OUT_ACCUMULATE if accumulate else 0)
             _ck(_lib.pgabb_vertex_triangles(self._h, ctypes.byref(o), out.data_ptr(), ctypes.byref(cnt)),
                 "pgabb_vertex_triangles")
             return out, (int(cnt.value) if sync else None)
@@ -231,7 +235,7 @@ class Blocks:
 
 def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = -1, rank: int = 0,
                  world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0,
-                 task_weights=None) -> Blocks:
+                 task_weights=None, reverse_order: bool = False) -> Blocks:
     """S1..S8: canonicalise, degree-order, orient, cut, block, enumerate, cost, assign.
 
     src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device).
@@ -248,6 +252,7 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     o.p, o.cut_rule, o.device = p, cut_rule, device
     o.inputs_on_device = int(sdev)
     o.rank, o.world_size, o.residency = rank, world_size, residency
+    o.reverse_order = int(bool(reverse_order))
     o.device_budget_bytes = device_budget_bytes
     tw = None
     if task_weights is not None:
@@ -262,6 +267,20 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     s = _abi.Stats()
     _ck(_lib.pgabb_get_stats(h, ctypes.byref(s)), "pgabb_get_stats")
     return Blocks(h, int(s.ntasks), int(s.p), int(n))
+
+
+def vertex_triangles_two_pass(n: int, src, dst, p: int = 0, **kw):
+    """t(v) for every original id by two cheap passes (DESIGN R24): the lowest and
+    middle vertex of every triangle from the forward handle (row totals and pair
+    counts: no per-hit atomics), the highest vertex as the LOWEST of the handle
+    built on the reversed degree order.  Returns (tv, T)."""
+    with build_blocks(n, src, dst, p=p, **kw) as f:
+        t1, T = f.vertex_triangles(roles="low+mid")
+    with build_blocks(n, src, dst, p=p, reverse_order=True, **kw) as r:
+        t2, T2 = r.vertex_triangles(roles="low")
+    if T2 != T:
+        raise RuntimeError(f"forward and reversed counts differ: {T} != {T2}")
+    return t1 + t2, T
 
 
 def triangle_count(n: int, src, dst, **kw) -> int:

@@ -25,11 +25,13 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ERANGE", 5: "EBUDGE
 RESIDENT_DEVICE, RESIDENT_HOST = 0, 1
 COUNT_ASYNC = 1
 OUT_DEVICE = 2
+ROLE_LOW, ROLE_MID, ROLE_HIGH = 4, 8, 16
+OUT_ACCUMULATE = 32
 
 
 class BuildOpts(ctypes.Structure):
     _fields_ = [("p", u32), ("cut_rule", u32), ("device", i32), ("inputs_on_device", u32),
-                ("rank", i32), ("world_size", i32), ("residency", u32), ("reserved0", u32),
+                ("rank", i32), ("world_size", i32), ("residency", u32), ("reverse_order", u32),
                 ("device_budget_bytes", u64), ("task_weights", u64p), ("n_task_weights", u64)]
 
 

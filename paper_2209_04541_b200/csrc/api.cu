@@ -139,6 +139,8 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->rank = o.rank;
         h->world_size = o.world_size;
         h->residency = o.residency;
+        if (o.reverse_order > 1) fail(PGABB_EINVAL, "reverse_order must be 0 or 1");
+        h->reverse_order = o.reverse_order;
         h->budget = o.device_budget_bytes;
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
         if (o.task_weights) h->task_weights.assign(o.task_weights, o.task_weights + o.n_task_weights);
@@ -194,6 +196,8 @@ pgabb_status_t pgabb_vertex_triangles(pgabb_blocks_t b, const pgabb_count_opts_t
     return guarded([&] {
         if (!b) fail(PGABB_EINVAL, "handle is NULL");
         if (!tv && b->n) fail(PGABB_EINVAL, "tv is NULL");
+        if (opts && (opts->flags & PGABB_OUT_ACCUMULATE) && !(opts->flags & PGABB_OUT_DEVICE))
+            fail(PGABB_EINVAL, "PGABB_OUT_ACCUMULATE needs PGABB_OUT_DEVICE");
         if (opts && (opts->flags & PGABB_COUNT_ASYNC) && !(opts->flags & PGABB_OUT_DEVICE))
             fail(PGABB_EINVAL, "PGABB_COUNT_ASYNC needs PGABB_OUT_DEVICE (a host tv is written synchronously)");
         DeviceGuard g(b->device);
@@ -205,7 +209,13 @@ pgabb_status_t pgabb_vertex_triangles(pgabb_blocks_t b, const pgabb_count_opts_t
             d_out = tmp.p;
         }
         bool wrote = false;
-        const uint64_t T = count_triangles(b, opts, &wrote, d_out);
+        const uint32_t roles = opts ? opts->flags & (PGABB_ROLE_LOW | PGABB_ROLE_MID | PGABB_ROLE_HIGH) : 0u;
+        int vm = 3;
+        if (roles == PGABB_ROLE_LOW) vm = 1;
+        else if (roles == (PGABB_ROLE_LOW | PGABB_ROLE_MID)) vm = 2;
+        else if (roles != 0 && roles != (PGABB_ROLE_LOW | PGABB_ROLE_MID | PGABB_ROLE_HIGH))
+            fail(PGABB_EINVAL, "roles must be LOW, LOW|MID or LOW|MID|HIGH");
+        const uint64_t T = count_triangles(b, opts, &wrote, d_out, nullptr, vm);
         if (!on_dev && b->n) {
             cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : b->stream;
             PG_CK(cudaMemcpyAsync(tv, d_out, (size_t)b->n * 8, cudaMemcpyDeviceToHost, st));

@@ -92,10 +92,10 @@ __global__ void k_iota(uint32_t* a, uint32_t n) {
         a[k] = (uint32_t)k;
 }
 
-__global__ void k_scatter_rank(const uint32_t* order, uint32_t n, uint32_t* rank) {
+__global__ void k_scatter_rank(const uint32_t* order, uint32_t n, uint32_t* rank, int reverse) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x)
-        rank[order[k]] = (uint32_t)k;
+        rank[order[k]] = reverse ? n - 1 - (uint32_t)k : (uint32_t)k;
 }
 
 // S3: relabel to rank space and orient low -> high.
@@ -408,6 +408,9 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_CK(cudaMemsetAsync(h->d_deg.p, 0, (size_t)std::max<uint32_t>(n, 1) * 4, st));
         if (n) {
             k_iota<<<grid_for(n), kThreads, 0, st>>>(h->d_rank.p, n);
+            if (h->reverse_order) {   // all degrees 0: the (deg, id) order is the id order
+                k_scatter_rank<<<grid_for(n), kThreads, 0, st>>>(h->d_rank.p, n, h->d_rank.p, 1);
+            }
             PG_LAUNCH_CHECK();
         }
         PG_CK(cudaStreamSynchronize(st));
@@ -483,7 +486,7 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         cub_call([&](void* t, size_t& b) {
             return cub::DeviceRadixSort::SortPairs(t, b, deg.p, deg2.p, ids.p, order.p, (int64_t)n, 0, 32, st);
         }, st, tmp);
-        k_scatter_rank<<<grid_for(n), kThreads, 0, st>>>(order.p, n, h->d_rank.p);
+        k_scatter_rank<<<grid_for(n), kThreads, 0, st>>>(order.p, n, h->d_rank.p, (int)h->reverse_order);
         PG_LAUNCH_CHECK();
         PG_CK(cudaStreamSynchronize(st));
         // deg(v) stays with the handle (local clustering coefficient, NEXT-1)

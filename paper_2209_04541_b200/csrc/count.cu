@@ -116,7 +116,11 @@ constexpr uint32_t kScratchWords = 96;                   // per-warp list descri
 // (1024 u16) and its hit counters (1024 u16), see VCnt
 constexpr uint32_t kVtxSlots = 1024;
 constexpr uint32_t kScratchWordsV = 128 + kVtxSlots / 2 + kVtxSlots / 2;
-__host__ __device__ constexpr uint32_t scratch_words(bool vtx) { return vtx ? kScratchWordsV : kScratchWords; }
+// VM (per-vertex roles, NEXT-1): 0 count only; 1 the row's lowest vertex u; 2 + the
+// middle vertex v (per pair); 3 + the highest vertex w (per hit, warp counters)
+__host__ __device__ constexpr uint32_t scratch_words(int vm) {
+    return vm >= 3 ? kScratchWordsV : vm >= 1 ? 128u : kScratchWords;
+}
 
 // Per-vertex counts, third vertex w (NEXT-1): a hub w is hit by many v of the same
 // row, so instead of one global atomic per hit the row's hits are counted in warp
@@ -217,7 +221,7 @@ __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 3
 // VTX (per-vertex counts, NEXT-1): each pair's count c_uv is also added to
 // tvj[v], and each common element w adds 1 to tvx[w]; the row total goes to u
 // in the caller.  VTX = false compiles to exactly the counting kernel.
-template <int MODE, int R, bool VTX>
+template <int MODE, int R, int VM>
 __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                   const uint32_t* __restrict__ rp_jx,
                                                   const uint32_t* __restrict__ Bc,
@@ -282,7 +286,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                         for (int r = 0; r < R; ++r) {
                             uint32_t wd = su[r] & wds[z][r];
                             cv += __popc(wd);
-                            if (VTX)
+                            if (VM >= 3)
                                 for (; wd; wd &= wd - 1u)
                                     vhit<0>(vc, S, 32u * (kl + r * 32) + (__ffs(wd) - 1), 0, 0);
                         }
@@ -292,12 +296,12 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                         for (uint32_t k = kl; k < W; k += gsz) {
                             uint32_t wd = S[k] & __ldg(row + (k - kl));
                             cv += __popc(wd);
-                            if (VTX)
+                            if (VM >= 3)
                                 for (; wd; wd &= wd - 1u) vhit<0>(vc, S, 32u * k + (__ffs(wd) - 1), 0, 0);
                         }
                     }
                     acc += cv;
-                    if (VTX && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
+                    if (VM >= 2 && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
                 }
             }
             if (use_and) lb = 0;
@@ -319,7 +323,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                             if (__ldg(Bc + b0 + mid) < ak) lo = mid + 1; else hi = mid;
                         }
                         const uint32_t hit = (lo < lb && __ldg(Bc + b0 + lo) == ak);
-                        if (VTX && hit) {
+                        if (VM >= 3 && hit) {
                             if (vc.on) vcnt_add(vc.cnt, MODE == 0 ? c + k : hash_find(S, ak, hbits, hmask));
                             else atomicAdd(vc.tvx + ak, 1ull);
                         }
@@ -328,7 +332,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 }
             }
             acc += cv;
-            if (VTX && cv) atomicAdd(tvj + v, (unsigned long long)cv);
+            if (VM >= 2 && cv) atomicAdd(tvj + v, (unsigned long long)cv);
             if (use_search) lb = 0;
             PROF_MARK(4);
         }
@@ -357,7 +361,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             scratch[sidx] = (lo >> 2) - excl;
             scratch[32 + sidx] = lo;
             scratch[64 + sidx] = hi;
-            if (VTX) scratch[96 + sidx] = v;
+            if (VM >= 2) scratch[96 + sidx] = v;
         }
         __syncwarp();
         for (uint32_t base = 0; base < total; base += 64) {
@@ -381,16 +385,16 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                     vpos[r] = pos + scratch[seg];
                     wlo[r] = scratch[32 + seg];
                     whi[r] = scratch[64 + seg];
-                    if (VTX) vv[r] = scratch[96 + seg];
+                    if (VM >= 2) vv[r] = scratch[96 + seg];
                     x[r] = __ldg(V + vpos[r]);
                 }
             }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int w0 = 4 * (int)vpos[r];
-                const uint32_t c = probe4<MODE, VTX>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, vc);
+                const uint32_t c = probe4<MODE, (VM >= 3)>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, vc);
                 acc += c;
-                if (VTX && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
+                if (VM >= 2 && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
             }
         }
         PROF_MARK(6);
@@ -402,7 +406,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
 // takes v_l and tests each element a of A_ix[u] (broadcast by shuffle) against
 // bit a of v_l's bitmap row.  Costs |A_ix[u]| bit tests per pair instead of W
 // word ANDs, and needs no staging of u at all.
-template <bool VTX>
+template <int VM>
 __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                     const uint32_t* __restrict__ A, uint32_t la,
                                                     const uint32_t* __restrict__ BM, uint32_t W, int lane,
@@ -425,13 +429,11 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
                 hit = (__ldg(BM + (uint64_t)v * W + (a >> 5)) >> (a & 31)) & 1u;
                 acc += hit;
             }
-            if (VTX) {   // lanes hitting the same w add once (warp-aggregated)
+            if (VM >= 3) {   // lanes hitting the same w add once (warp-aggregated)
                 const uint32_t same = __match_any_sync(0xffffffffu, hit ? a : 0xffffffffu);
-                if (hit) {
-                    if (lane == __ffs(same) - 1) atomicAdd(tvx + a, (unsigned long long)__popc(same));
-                    atomicAdd(tvj + v, 1ull);
-                }
+                if (hit && lane == __ffs(same) - 1) atomicAdd(tvx + a, (unsigned long long)__popc(same));
             }
+            if (VM >= 2 && hit) atomicAdd(tvj + v, 1ull);
             q += dq;
             k += dk;
             if (k >= la) {
@@ -459,7 +461,7 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
                 for (int z = 0; z < kDenseUnroll; ++z) {
                     const uint32_t hit = (wv[z] >> (ak[z] & 31)) & 1u;
                     cv += hit;
-                    if (VTX && k + z < m) {   // one atomic per element for the whole warp's v's
+                    if (VM >= 3 && k + z < m) {   // one atomic per element for the whole warp's v's
                         const uint32_t mk = __ballot_sync(0xffffffffu, hit);
                         if (lane == 0 && mk) atomicAdd(tvx + ak[z], (unsigned long long)__popc(mk));
                     }
@@ -467,7 +469,7 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
             }
         }
         acc += cv;
-        if (VTX && cv) atomicAdd(tvj + v, (unsigned long long)cv);
+        if (VM >= 2 && cv) atomicAdd(tvj + v, (unsigned long long)cv);
     }
     return acc;
 }
@@ -528,7 +530,7 @@ __device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next
 // found here that contain the vertex -- u gets the row total, v each pair's
 // c_uv, w one per hit -- so sum over ranks of tv = t(v) and sum tv = 3T.
 // TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
-template <bool IMPLICIT, bool VTX, bool TIMED>
+template <bool IMPLICIT, int VM, bool TIMED>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
           unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
@@ -538,12 +540,12 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* S = smem + wid * (kSetWords + scratch_words(VTX));
+    uint32_t* S = smem + wid * (kSetWords + scratch_words(VM));
     uint32_t* scratch = S + kSetWords;
     uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt)
     uint32_t* vcnt = vpre + kVtxSlots / 2;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
-    if (VTX)
+    if (VM >= 3)
         for (uint32_t k = lane; k < kVtxSlots / 2; k += 32) vcnt[k] = 0;   // invariant: zero between rows
     __syncwarp();
     // Warps claim kRowChunk items at a time from one counter, so the items in
@@ -588,12 +590,12 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         const uint32_t hbits = max(5, 32 - __clz(2 * la - 1));   // smallest 2^hbits >= 2 la (>= 32)
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
-        unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
-        unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
+        unsigned long long* tvj = VM > 0 ? tv + T.cj : nullptr;
+        unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
         VCnt vc{vcnt, vpre, tvx, false};
         PROF_MARK(0);
         if (T.bm_jx != ~0ull && 8 * la <= kDenseRowMul * T.bm_words) {
-            acc = probe_dense_row<VTX>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
+            acc = probe_dense_row<VM>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);
         } else if (mode == 0) {
@@ -602,7 +604,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 atomicOr(&S[w >> 5], 1u << (w & 31));
             }
             __syncwarp();
-            if (VTX && la <= kVtxSlots && e1 - e0 < 65536u) {
+            if (VM >= 3 && la <= kVtxSlots && e1 - e0 < 65536u) {
                 // prefix popcounts of S per word (u16): rank of a member w = pre[w>>5] + popc below it
                 vc.on = true;
                 const uint32_t W = (T.wx + 31) / 32;
@@ -627,14 +629,14 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             if (T.bm_jx != ~0ull) {
                 const uint32_t* BM = bitmap + T.bm_jx;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = intersect_row<0, 1, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
-                else if (W <= 128) acc = intersect_row<0, 4, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
-                else acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                if (W <= 32) acc = intersect_row<0, 1, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else if (W <= 128) acc = intersect_row<0, 4, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else acc = intersect_row<0, 0, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             } else {
-                acc = intersect_row<0, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                acc = intersect_row<0, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             }
             __syncwarp();
-            if (VTX && vc.on) {   // flush the row's w counters: one atomic per distinct w
+            if (VM >= 3 && vc.on) {   // flush the row's w counters: one atomic per distinct w
                 const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
                 for (uint32_t k = lane; k < la; k += 32) {
                     const uint32_t c = c16[k];
@@ -651,12 +653,12 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
-            if (VTX) vc.on = e1 - e0 < 65536u;   // slots <= 2 * kHashMaxList = kVtxSlots
+            if (VM >= 3) vc.on = e1 - e0 < 65536u;   // slots <= 2 * kHashMaxList = kVtxSlots
             PROF_MARK(2);
             PROF_CNT(18);
-            acc = intersect_row<1, 0, VTX>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+            acc = intersect_row<1, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
             __syncwarp();
-            if (VTX && vc.on) {
+            if (VM >= 3 && vc.on) {
                 const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
                 for (uint32_t k = lane; k <= hmask; k += 32) {
                     const uint32_t c = c16[k];
@@ -671,8 +673,8 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 const uint32_t v = __ldg(vcol + e);
                 const uint32_t b0 = __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
                 if (b1 > b0) {
-                    const uint32_t c = warp_intersect<VTX>(A, la, Bc + b0, b1 - b0, lane, tvx);
-                    if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+                    const uint32_t c = warp_intersect<(VM >= 3)>(A, la, Bc + b0, b1 - b0, lane, tvx);
+                    if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
                     acc += c;
                 }
             }
@@ -690,7 +692,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             acc_t = 0;
         }
         acc_t += sum;
-        if (VTX && lane == 0 && sum) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
+        if (VM >= 1 && lane == 0 && sum) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
         if (TIMED && lane == 0) atomicAdd(&cyc[t], (unsigned long long)(clock64() - c0));
         PROF_MARK(7);
     }
@@ -733,7 +735,7 @@ constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
 // IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
 // wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
 // it is light by k_row_flags's predicate (the heavy kernel skips exactly those).
-template <bool VTX, bool TIMED, bool IMPLICIT>
+template <int VM, bool TIMED, bool IMPLICIT>
 __global__ void __launch_bounds__(kLightThreads, PGABB_LIGHT_MINB)
 k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, int nwp, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
@@ -797,8 +799,8 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
         uint32_t a[kLightLa];
 #pragma unroll
         for (int k = 0; k < (int)kLightLa; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
-        unsigned long long* tvj = VTX ? tv + T.cj : nullptr;
-        unsigned long long* tvx = VTX ? tv + T.cx : nullptr;
+        unsigned long long* tvj = VM > 0 ? tv + T.cj : nullptr;
+        unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
         uint32_t acc = 0;
         if (bm_jx != ~0ull) {
             const uint32_t W = T.bm_words;
@@ -811,11 +813,11 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                 for (int k = 0; k < (int)kLightLa; ++k)
                     if (k < (int)la) {
                         const uint32_t hit = (__ldg(row + (a[k] >> 5)) >> (a[k] & 31)) & 1u;
-                        if (VTX && hit) atomicAdd(tvx + a[k], 1ull);
+                        if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
                         c += hit;
                     }
                 acc += c;
-                if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+                if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
             }
         } else {
             const uint64_t rp_jx = T.rp_jx;
@@ -831,7 +833,7 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                         uint32_t hit = 0;
 #pragma unroll
                         for (int k = 0; k < (int)kLightLa; ++k) hit |= (x == a[k]);
-                        if (VTX && hit) atomicAdd(tvx + x, 1ull);
+                        if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
                         c += hit;
                     }
                 } else {
@@ -844,16 +846,16 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                                 if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
                             }
                             const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
-                            if (VTX && hit) atomicAdd(tvx + a[k], 1ull);
+                            if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
                             c += hit;
                         }
                 }
                 acc += c;
-                if (VTX && c) atomicAdd(tvj + v, (unsigned long long)c);
+                if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
             }
         }
         acc_t += acc;
-        if (VTX && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
+        if (VM >= 1 && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
         if (TIMED) cyc_t += (unsigned long long)(clock64() - c0);
     }
     }
@@ -880,10 +882,11 @@ __global__ void k_sum_tasks(unsigned long long* tc, int nt, unsigned long long* 
 }
 
 // Per-vertex counts back to original ids: tv[v] = tv_rank[rank[v]].
+// accumulate: tv[v] += (PGABB_OUT_ACCUMULATE, the second pass of the two-pass route)
 __global__ void k_gather_tv(const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ tv_rank,
-                            uint32_t n, unsigned long long* __restrict__ tv) {
+                            uint32_t n, unsigned long long* __restrict__ tv, int accumulate) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        tv[v] = tv_rank[rank[v]];
+        tv[v] = (accumulate ? tv[v] : 0ull) + tv_rank[rank[v]];
 }
 
 // Local clustering coefficient (NEXT-1): cc(v) = 2 t(v) / (deg(v) (deg(v) - 1)),
@@ -927,7 +930,7 @@ namespace pgabb {
 #endif
 
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
-                         unsigned long long* d_tv_out, unsigned long long* d_cycles) {
+                         unsigned long long* d_tv_out, unsigned long long* d_cycles, int vm) {
     const bool timed = d_cycles != nullptr;   // pgabb_task_times: counting kernels with cycle accounting
     cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
     const bool async = opts && (opts->flags & PGABB_COUNT_ASYNC);
@@ -936,27 +939,32 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     h->h2d_last = 0;
     h->d2d_last = 0;
 
-    const bool vtx = d_tv_out != nullptr;
+    if (d_tv_out == nullptr) vm = 0;   // vm: per-vertex roles level (scratch_words)
+    const bool vtx = vm > 0;
     h->light_timed = false;
-    const size_t smem = kRowWarps * (kSetWords + scratch_words(vtx)) * sizeof(uint32_t);
-    static thread_local int cached_dev = -1, grid_c = 0, grid_v = 0;
+    const size_t smem = kRowWarps * (kSetWords + scratch_words(vm)) * sizeof(uint32_t);
+    static thread_local int cached_dev = -1, grids[4] = {0, 0, 0, 0};
     if (cached_dev != h->device) {
-        const size_t sm_c = kRowWarps * (kSetWords + scratch_words(false)) * sizeof(uint32_t);
-        const size_t sm_v = kRowWarps * (kSetWords + scratch_words(true)) * sizeof(uint32_t);
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
-        PG_CK(cudaFuncSetAttribute(k_tc_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
         int sms = 0, per_sm = 0;
         PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, false, false>, kRowWarps * 32, sm_c));
-        grid_c = sms * std::max(per_sm, 1);
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_rows<false, true, false>, kRowWarps * 32, sm_v));
-        grid_v = sms * std::max(per_sm, 1);
+        auto setup = [&](auto kfn, int level) {
+            const size_t sm = kRowWarps * (kSetWords + scratch_words(level)) * sizeof(uint32_t);
+            PG_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kRowWarps * 32, sm));
+            return sms * std::max(per_sm, 1);
+        };
+        grids[0] = setup(k_tc_rows<false, 0, false>, 0);
+        setup(k_tc_rows<true, 0, false>, 0);
+        setup(k_tc_rows<false, 0, true>, 0);
+        grids[1] = setup(k_tc_rows<false, 1, false>, 1);
+        setup(k_tc_rows<true, 1, false>, 1);
+        grids[2] = setup(k_tc_rows<false, 2, false>, 2);
+        setup(k_tc_rows<true, 2, false>, 2);
+        grids[3] = setup(k_tc_rows<false, 3, false>, 3);
+        setup(k_tc_rows<true, 3, false>, 3);
         cached_dev = h->device;
     }
-    const int grid = vtx ? grid_v : grid_c;
+    const int grid = grids[vm];
     auto grid_for_items = [&](unsigned long long n) {
         return (unsigned)std::max(1ull, std::min<unsigned long long>((unsigned long long)grid,
                                                                      (n + kRowWarps - 1) / kRowWarps));
@@ -967,9 +975,22 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         tv = h->d_tv_rank.p;
     }
     auto rows_kernel = [&](bool implicit) {
-        if (implicit) return vtx ? k_tc_rows<true, true, false> : k_tc_rows<true, false, false>;
-        if (timed) return k_tc_rows<false, false, true>;
-        return vtx ? k_tc_rows<false, true, false> : k_tc_rows<false, false, false>;
+        if (timed) return k_tc_rows<false, 0, true>;
+        switch (vm) {
+            case 1: return implicit ? k_tc_rows<true, 1, false> : k_tc_rows<false, 1, false>;
+            case 2: return implicit ? k_tc_rows<true, 2, false> : k_tc_rows<false, 2, false>;
+            case 3: return implicit ? k_tc_rows<true, 3, false> : k_tc_rows<false, 3, false>;
+            default: return implicit ? k_tc_rows<true, 0, false> : k_tc_rows<false, 0, false>;
+        }
+    };
+    auto light_kernel = [&](bool implicit) {
+        if (timed) return k_tc_light<0, true, false>;
+        switch (vm) {
+            case 1: return implicit ? k_tc_light<1, false, true> : k_tc_light<1, false, false>;
+            case 2: return implicit ? k_tc_light<2, false, true> : k_tc_light<2, false, false>;
+            case 3: return implicit ? k_tc_light<3, false, true> : k_tc_light<3, false, false>;
+            default: return implicit ? k_tc_light<0, false, true> : k_tc_light<0, false, false>;
+        }
     };
 
     PG_CK(cudaEventRecord(h->ev0, st));
@@ -999,16 +1020,14 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             if (light_dev != h->device) {
                 int sms = 0, per_sm = 0;
                 PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<false, false, false>,
+                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false, false>,
                                                                     kLightThreads, 0));
                 light_grid = sms * std::max(per_sm, 1);
                 light_dev = h->device;
             }
             const unsigned g = (unsigned)std::max<unsigned long long>(
                 1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
-            (timed ? k_tc_light<false, true, false> : vtx ? k_tc_light<true, false, false>
-                                                          : k_tc_light<false, false, false>)
-                <<<g, kLightThreads, 0, st>>>(h->d_light.p, nullptr, 0, h->n_light, h->d_tasks.p, h->d_col.p,
+            light_kernel(false)<<<g, kLightThreads, 0, st>>>(h->d_light.p, nullptr, 0, h->n_light, h->d_tasks.p, h->d_col.p,
                                               h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p, tv, h->d_next.p,
                                               timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
@@ -1051,7 +1070,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             {
                 const unsigned lg = (unsigned)std::max<unsigned long long>(
                     1ull, std::min<unsigned long long>(148ull * 8, (wv.rows + kLightThreads - 1) / kLightThreads));
-                (vtx ? k_tc_light<true, false, true> : k_tc_light<false, false, true>)<<<lg, kLightThreads, 0, st>>>(
+                light_kernel(true)<<<lg, kLightThreads, 0, st>>>(
                     nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
                     h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv,
                     h->d_next.p + 3, nullptr);
@@ -1067,7 +1086,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     h->launches_last++;
     if (vtx && h->n) {
         k_gather_tv<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, 148 * 16), 256, 0, st>>>(
-            h->d_rank.p, tv, h->n, d_tv_out);
+            h->d_rank.p, tv, h->n, d_tv_out, (opts && (opts->flags & PGABB_OUT_ACCUMULATE)) ? 1 : 0);
         PG_LAUNCH_CHECK();
         h->launches_last++;
     }

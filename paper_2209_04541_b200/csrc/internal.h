@@ -211,6 +211,7 @@ struct pgabb_blocks_s {
     uint32_t cut_rule = 0;
     int32_t rank = 0, world_size = 1;
     uint32_t residency = PGABB_RESIDENT_DEVICE;
+    uint32_t reverse_order = 0;                 // S2 ranks reversed (DESIGN R24)
     uint64_t budget = 0;
     uint64_t wedges = 0;
 
@@ -273,7 +274,8 @@ void plan_pieces(pgabb_blocks_s* h);
 void upload_work(pgabb_blocks_s* h);
 void plan_waves(pgabb_blocks_s* h);
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
-                         unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr);
+                         unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr,
+                         int vm = 3);
 void task_times(pgabb_blocks_s* h, uint64_t* ns);
 void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uint32_t* labels, uint64_t* ncomp,
                           uint32_t* iters);

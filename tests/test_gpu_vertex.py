@@ -16,6 +16,7 @@ import pytest
 
 import gen
 import oracle
+import oracle.blocks as ob
 
 pytestmark = pytest.mark.gpu
 
@@ -128,3 +129,52 @@ def test_per_vertex_messy_input():
     with pg.build_blocks(*m, p=3) as b:
         tv, _ = b.vertex_triangles()
     assert np.array_equal(tv, want)
+
+
+# ---- roles and the two-pass route (DESIGN R24) -------------------------------------
+@pytest.mark.parametrize("p", [1, 3, 8])
+def test_roles_vs_oracle(p):
+    for g in (gen.rmat(12, 16, seed=30 + p), gen.disjoint_union(gen.complete(60), gen.king(20, 30))):
+        T, lo, mi, hi = oracle.count_roles(*g)
+        with pg.build_blocks(*g, p=p) as b:
+            t_lo, T1 = b.vertex_triangles(roles="low")
+            t_lm, T2 = b.vertex_triangles(roles="low+mid")
+        assert T1 == T2 == T
+        assert np.array_equal(t_lo, lo)
+        assert np.array_equal(t_lm - t_lo, mi)
+        with pg.build_blocks(*g, p=p, reverse_order=True) as r:
+            assert r.triangle_count() == T                       # reversal keeps T
+            rt_lo, _ = r.vertex_triangles(roles="low")
+            rt_all, _ = r.vertex_triangles()
+        assert np.array_equal(rt_lo, hi)                          # lowest in reverse = highest
+        assert np.array_equal(rt_all, lo + mi + hi)
+
+
+def test_two_pass_vertex_triangles():
+    for g, p in ((gen.rmat(14, 16, seed=41), 8), (gen.er(1 << 13, 24, seed=42), 4), (gen.grid(150, 0.4, seed=43), 5)):
+        _, want = oracle.count(*g, per_vertex=True)
+        tv, T = pg.vertex_triangles_two_pass(*g, p=p)
+        assert np.array_equal(tv, want) and int(tv.sum()) == 3 * T
+
+
+def test_reverse_order_steps_parity():
+    g = gen.rmat(9, 16, seed=44)
+    P = ob.Plan(*g, p=3, reverse=True)
+    with pg.build_blocks(*g, p=3, reverse_order=True) as b:
+        assert (b.rank() == P.rank).all()
+        assert list(b.cuts()) == list(P.cuts)
+        ijx, cost, alg = b.tasks()
+        assert [tuple(map(int, t)) for t in ijx] == P.tasks
+        assert list(map(int, cost)) == P.costs
+        T, tc = b.triangle_count(task_counts=True)
+        assert list(map(int, tc)) == P.task_counts()
+
+
+def test_bad_roles_rejected():
+    g = gen.rmat(8, 8, seed=45)
+    with pg.build_blocks(*g, p=2) as b:
+        o = pg._abi.CountOpts()
+        o.flags = pg._abi.ROLE_MID
+        tv = np.zeros(g[0], np.uint64)
+        import ctypes
+        assert pg._lib.pgabb_vertex_triangles(b._h, ctypes.byref(o), tv.ctypes.data, None) == 1

@@ -281,3 +281,21 @@ def test_components_closed_forms():
     assert nc == 6 and lab.tolist() == list(range(6))
     lab, nc = oracle.components(*gen.messy(gen.cycle(50), seed=3))   # noise does not change G_s
     assert nc == 1
+
+
+# ---- per-vertex counts by role (DESIGN R24) --------------------------------------
+def test_roles_sum_and_closed_form():
+    for g in (gen.rmat(10, 16, seed=8), gen.king(8, 9), gen.er_small(150, 0.1, seed=9)):
+        T, lo, mi, hi = oracle.count_roles(*g)
+        T2, tv = oracle.count(*g, per_vertex=True)
+        assert T == T2
+        assert np.array_equal(lo + mi + hi, tv)
+        assert int(lo.sum()) == int(mi.sum()) == int(hi.sum()) == T   # one vertex of each role
+    # K_n: all degrees equal, so the order is by id; vertex r is lowest in C(n-1-r, 2)
+    # triangles, middle in r(n-1-r), highest in C(r, 2)
+    n = 13
+    T, lo, mi, hi = oracle.count_roles(*gen.complete(n))
+    r = np.arange(n)
+    assert (lo == (n - 1 - r) * (n - 2 - r) // 2).all()
+    assert (mi == r * (n - 1 - r)).all()
+    assert (hi == r * (r - 1) // 2).all()
