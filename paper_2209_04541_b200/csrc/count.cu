@@ -67,17 +67,17 @@ __device__ __forceinline__ uint32_t warp_intersect(const uint32_t* __restrict__ 
 //            a bitmap of w_x bits (w_x <= 32768, 4 KB) or, for wider parts, an
 //            open-addressing hash of <= 1024 slots (|A_ix[u]| <= 512);
 //   stream   the lists A_jx[v] of 32 consecutive v in A_ij[u] at a time, as
-//            one flattened sequence: lane l takes positions l, l+32, ... and
-//            finds its v by a 5-step shuffle search over the warp's prefix of
-//            list lengths, so short lists do not idle lanes (load-balanced
-//            "merge-path" over the batch); reads are coalesced within a list;
+//            one flattened sequence of 16-byte covers (see intersect_row), so
+//            short lists do not idle lanes; dense A_jx rows are ANDed with the
+//            staged bitmap, short-vs-long pairs binary-searched;
 //   probe    each element against the staged set;
-//   reduce   lane partials -> warp sum -> one atomicAdd into the task's count.
+//   reduce   lane partials -> warp sum, kept per warp while consecutive rows
+//            share a task, one atomicAdd per task change.
 //
-// Rows whose A_ix[u] fits neither set fall back to lane-parallel binary search.
-// This is the staged model of SURVEY §8(d): A_ix[u] read once per (task, u),
-// A_jx[v] once per edge.  Items arrive sorted by estimated work (heaviest
-// first) and are dealt cyclically to the warps of the grid (no atomics).
+// Rows whose A_ix[u] fits neither set fall back to lane-parallel binary search;
+// dense A_jx with a short A_ix[u] skips staging (probe_dense_row).  This is the
+// staged model of SURVEY §8(d): A_ix[u] read once per (task, u), A_jx[v] once
+// per edge.  Items are in locality order and claimed by warps from a counter.
 // ---------------------------------------------------------------------------
 constexpr int kRowWarps = 8;
 #ifndef PGABB_AND_UNROLL
@@ -218,9 +218,9 @@ __device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int
 
 __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
-// VTX (per-vertex counts, NEXT-1): each pair's count c_uv is also added to
-// tvj[v], and each common element w adds 1 to tvx[w]; the row total goes to u
-// in the caller.  VTX = false compiles to exactly the counting kernel.
+// VM (per-vertex roles, NEXT-1): VM >= 2 adds each pair's count c_uv to tvj[v],
+// VM >= 3 counts each common element w for w (warp counters, VCnt); the row
+// total goes to u in the caller (VM >= 1).  VM = 0 is exactly the counting kernel.
 template <int MODE, int R, int VM>
 __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
                                                   const uint32_t* __restrict__ rp_jx,
@@ -524,11 +524,12 @@ __device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next
 
 // IMPLICIT = false: items[] holds the compacted row items (device-resident blocks).
 // IMPLICIT = true (streaming residency): item idx is row idx of the wave's piece
-// table wp[0..nwp) (rows of empty lists are skipped in the kernel), and the pool
-// pointers all point at the wave's staging arena.
-// VTX = true (per-vertex counts, NEXT-1): tv[rank-space id] += the triangles
-// found here that contain the vertex -- u gets the row total, v each pair's
-// c_uv, w one per hit -- so sum over ranks of tv = t(v) and sum tv = 3T.
+// table wp[0..nwp) (empty and light rows are dropped by implicit_heavy_rows), and
+// the pool pointers all point at the wave's staging arena.
+// VM > 0 (per-vertex counts, NEXT-1): tv[rank-space id] += the triangles found
+// here that contain the vertex in the requested roles -- u gets the row total
+// (VM >= 1), v each pair's c_uv (VM >= 2), w one per hit (VM >= 3) -- so with
+// VM = 3 the sum over ranks of tv is t(v) and sum tv = 3T.
 // TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
 template <bool IMPLICIT, int VM, bool TIMED>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
