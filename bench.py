@@ -332,6 +332,10 @@ def run_ours(args):
         comm.barrier()
     step_ms = [a.elapsed_time(z) for a, z in ev]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    # per-rank step time (balance evidence): rank r's slot, summed over ranks
+    per_rank = torch.zeros(ws, dtype=torch.float64, device="cuda")
+    per_rank[rank] = sum(step_ms) / args.steps
+    per_rank_ms = [float(x) for x in comm.allreduce_(per_rank).cpu()]
     tot_ms = float(comm.allreduce_(tot, "max").item())       # max over ranks
     ms_per_step = tot_ms / args.steps
     value = m_edges / (ms_per_step / 1e3)
@@ -408,6 +412,7 @@ def run_ours(args):
                        "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
                        "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
                        "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}", "balance": args.balance if ws > 1 else None,
+                       "per_rank_ms": per_rank_ms,
                        "comm": comm.backend,
                        "residency": (f"host-streamed through a {args.budget_gb:g} GB device budget, "
                                      f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B + D2D reuse "
