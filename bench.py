@@ -403,8 +403,6 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC if not vertex else "per-vertex triangle-count edges/sec (|E|/time)",
-            "vertex_route": ("two-pass (low+mid forward, low reversed; R24)" if b_rev is not None
-                             else "one-pass (all roles)") if vertex else None,
             "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -426,6 +424,9 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if vertex:
+            line["vertex_route"] = ("two-pass (low+mid forward, low reversed; R24)" if b_rev is not None
+                                    else "one-pass (all roles)")
         gold = golden_triangles(args.config)
         if cpu and cpu.get("full"):
             line["parity"] = {"oracle_triangles": cpu["triangles_in_sample"],
