@@ -114,8 +114,16 @@ constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per 
 constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
 // per-vertex kernel: + the batch's v ids (32), the row's prefix popcounts of S
 // (1024 u16) and its hit counters (1024 u16), see VCnt
-constexpr uint32_t kVtxSlots = 1024;
-constexpr uint32_t kScratchWordsV = 128 + kVtxSlots / 2 + kVtxSlots / 2;
+#ifndef PGABB_VTX_SLOTS
+#define PGABB_VTX_SLOTS 1024
+#endif
+#ifndef PGABB_VTX_PRE_GROUP
+#define PGABB_VTX_PRE_GROUP 1   // A/B: 8 (4 CTAs/SM) is 1.5x slower: extra popcounts per hit
+#endif
+constexpr uint32_t kVtxSlots = PGABB_VTX_SLOTS;        // u16 hit counters per warp
+constexpr uint32_t kPreGroup = PGABB_VTX_PRE_GROUP;    // S words per stored prefix popcount
+constexpr uint32_t kPreWords = (kSetWords / kPreGroup + 1) / 2;
+constexpr uint32_t kScratchWordsV = 128 + kPreWords + kVtxSlots / 2;
 // VM (per-vertex roles, NEXT-1): 0 count only; 1 the row's lowest vertex u; 2 + the
 // middle vertex v (per pair); 3 + the highest vertex w (per hit, warp counters)
 __host__ __device__ constexpr uint32_t scratch_words(int vm) {
@@ -131,7 +139,7 @@ __host__ __device__ constexpr uint32_t scratch_words(int vm) {
 // global atomic per hit.
 struct VCnt {
     uint32_t* cnt;                     // u16 x kVtxSlots, packed in pairs
-    uint32_t* pre;                     // u16 x kVtxSlots: popcount of S[0..k) (bitmap mode)
+    uint32_t* pre;                     // u16 per kPreGroup words of S: popcount of S[0..g*kPreGroup)
     unsigned long long* tvx;           // global t(v) of part x
     bool on;
 };
@@ -141,7 +149,10 @@ __device__ __forceinline__ void vcnt_add(uint32_t* cnt, uint32_t idx) {
 __device__ __forceinline__ uint32_t u16_at(const uint32_t* a, uint32_t k) { return (a[k >> 1] >> ((k & 1u) << 4)) & 0xffffu; }
 // rank of w (a member of the bitmap set S) among the set's elements
 __device__ __forceinline__ uint32_t rank_in_set(const uint32_t* S, const uint32_t* pre, uint32_t w) {
-    return u16_at(pre, w >> 5) + __popc(S[w >> 5] & ((1u << (w & 31)) - 1u));
+    const uint32_t k = w >> 5, g0 = k - k % kPreGroup;
+    uint32_t r = u16_at(pre, k / kPreGroup) + __popc(S[k] & ((1u << (w & 31)) - 1u));
+    for (uint32_t z = g0; z < k; ++z) r += __popc(S[z]);
+    return r;
 }
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
@@ -544,7 +555,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     uint32_t* S = smem + wid * (kSetWords + scratch_words(VM));
     uint32_t* scratch = S + kSetWords;
     uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt)
-    uint32_t* vcnt = vpre + kVtxSlots / 2;
+    uint32_t* vcnt = vpre + kPreWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     if (VM >= 3)
         for (uint32_t k = lane; k < kVtxSlots / 2; k += 32) vcnt[k] = 0;   // invariant: zero between rows
@@ -606,21 +617,24 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             }
             __syncwarp();
             if (VM >= 3 && la <= kVtxSlots && e1 - e0 < 65536u) {
-                // prefix popcounts of S per word (u16): rank of a member w = pre[w>>5] + popc below it
+                // prefix popcounts of S per group of kPreGroup words (u16): the rank of a
+                // member w is pre[group] + the popcounts of the words before it in its group
                 vc.on = true;
-                const uint32_t W = (T.wx + 31) / 32;
+                const uint32_t W = (T.wx + 31) / 32, NG = (W + kPreGroup - 1) / kPreGroup;
                 uint16_t* pre16 = reinterpret_cast<uint16_t*>(vpre);
                 uint32_t run = 0;
-                for (uint32_t b = 0; b < W; b += 32) {
-                    const uint32_t k = b + lane;
-                    const uint32_t c = k < W ? __popc(S[k]) : 0u;
+                for (uint32_t b = 0; b < NG; b += 32) {
+                    const uint32_t g = b + lane;
+                    uint32_t c = 0;
+                    if (g < NG)
+                        for (uint32_t z = g * kPreGroup; z < min(W, (g + 1) * kPreGroup); ++z) c += __popc(S[z]);
                     uint32_t incl = c;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                         if (lane >= o) incl += y;
                     }
-                    if (k < W) pre16[k] = (uint16_t)(run + incl - c);
+                    if (g < NG) pre16[g] = (uint16_t)(run + incl - c);
                     run += __shfl_sync(0xffffffffu, incl, 31);
                 }
                 __syncwarp();
@@ -654,7 +668,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
             }
             __syncwarp();
-            if (VM >= 3) vc.on = e1 - e0 < 65536u;   // slots <= 2 * kHashMaxList = kVtxSlots
+            if (VM >= 3) vc.on = e1 - e0 < 65536u && hmask < kVtxSlots;   // one counter per hash slot
             PROF_MARK(2);
             PROF_CNT(18);
             acc = intersect_row<1, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
