@@ -740,12 +740,16 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
 // ---------------------------------------------------------------------------
 constexpr int kLightThreads = 256;
 #ifndef PGABB_LIGHT_MINB
-#define PGABB_LIGHT_MINB 8   // 8 x 256 threads per SM (32 registers): measured best on c3
+#define PGABB_LIGHT_MINB 6   // 6 x 256 threads per SM (40 registers, with the item prefetch): A/B best on c2/c3/c4
 #endif
 #ifndef PGABB_LIGHT_CHUNK
 #define PGABB_LIGHT_CHUNK 8
 #endif
 constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
+#ifndef PGABB_LIGHT_PREFETCH
+#define PGABB_LIGHT_PREFETCH 1
+#endif
+constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
 
 // IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
 // wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
@@ -765,6 +769,8 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
     if (lane == 0) base = atomicAdd(next, (unsigned long long)(32 * kLightChunk));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= nitems) break;
+    uint4 it_next = make_uint4(0, 0, 0, 0);   // PGABB_LIGHT_PREFETCH: the next item, loaded a step early
+    if (!IMPLICIT && kLightPrefetch && base + lane < nitems) it_next = __ldg(items + base + lane);
     for (int r = 0; r < kLightChunk; ++r) {
         const unsigned long long idx = base + 32 * r + lane;
         if (idx >= nitems) break;
@@ -792,7 +798,13 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                 if (work > kLightWork) continue;   // a heavy row: the warp kernel's
             }
         } else {
-            const uint4 it = __ldg(items + idx);
+            uint4 it;
+            if (kLightPrefetch) {
+                it = it_next;
+                if (r + 1 < kLightChunk && idx + 32 < nitems) it_next = __ldg(items + idx + 32);
+            } else {
+                it = __ldg(items + idx);
+            }
             t = it.x & ((1u << kLightTaskBits) - 1);
             u = it.w;
             la = (it.x >> kLightTaskBits) & 15u;
