@@ -249,3 +249,20 @@ def test_task_times_drive_a_balanced_plan():
     with pytest.raises(pg.PgabbError) as e:
         pg.build_blocks(*g, p=8, task_weights=ns[:-1])
     assert e.value.name == "EINVAL"
+
+
+# ---------------------------------------------------------------- size limits
+def test_max_parts_and_clamp():
+    g = gen.rmat(12, 16, seed=51)
+    T = oracle.count(*g)
+    with pg.build_blocks(*g, p=64) as b:                 # kMaxParts: C(66,3) = 45760 candidate triples
+        assert b.stats()["p"] == 64
+        assert b.triangle_count() == T
+        ijx, _, _ = b.tasks()
+        assert all(i <= j <= x < 64 for i, j, x in ijx)
+    with pytest.raises(pg.PgabbError) as e:
+        pg.build_blocks(*g, p=65)
+    assert e.value.name == "EINVAL"
+    small = gen.complete(5)
+    with pg.build_blocks(*small, p=40) as b:             # p > n is clamped to n (R7)
+        assert b.stats()["p"] == 5 and b.triangle_count() == 10
