@@ -121,6 +121,10 @@ constexpr uint32_t kScratchWords = 96;                   // per-warp list descri
 #define PGABB_VTX_PRE_GROUP 1   // A/B: 8 (4 CTAs/SM) is 1.5x slower: extra popcounts per hit
 #endif
 constexpr uint32_t kVtxSlots = PGABB_VTX_SLOTS;        // u16 hit counters per warp
+#ifndef PGABB_HASH_FILTER
+#define PGABB_HASH_FILTER 1
+#endif
+constexpr bool kHashFilter = PGABB_HASH_FILTER;
 constexpr uint32_t kPreGroup = PGABB_VTX_PRE_GROUP;    // S words per stored prefix popcount
 constexpr uint32_t kPreWords = (kSetWords / kPreGroup + 1) / 2;
 constexpr uint32_t kScratchWordsV = 128 + kPreWords + kVtxSlots / 2;
@@ -159,9 +163,20 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t hbits) {
     return (w * 2654435761u) >> (32 - hbits);
 }
 
+// MODE 3 = the hash set of MODE 1 (<= kFilterSlots slots, words [0, 512) of S) plus
+// a 16384-bit filter over a second hash of w in words [512, 1024): most probes
+// of an intersection miss, and a miss usually costs one filter bit instead of a
+// walk along the open-addressing run.
+constexpr uint32_t kFilterSlots = kSetWords / 2;
+__device__ __forceinline__ uint32_t filter_bit(uint32_t w) { return (w * 0x9E3779B1u) >> 18; }   // 14 bits
+
 template <int MODE>
 __device__ __forceinline__ uint32_t probe(const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask) {
     if (MODE == 0) return (S[w >> 5] >> (w & 31)) & 1u;
+    if (MODE == 3) {
+        const uint32_t f = filter_bit(w);
+        if (!((S[kFilterSlots + (f >> 5)] >> (f & 31)) & 1u)) return 0u;
+    }
     uint32_t h = hash_slot(w, hbits), s;
     while ((s = S[h]) != 0u && s != w + 1) h = (h + 1) & hmask;
     return s == w + 1;
@@ -662,16 +677,28 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             }
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
         } else if (mode == 1) {
+            const bool filt = kHashFilter && hmask < kFilterSlots;
             for (uint32_t k = lane; k < la; k += 32) {
                 const uint32_t w = __ldg(A + k);
                 uint32_t h = hash_slot(w, hbits);
                 while (atomicCAS(&S[h], 0u, w + 1) != 0u) h = (h + 1) & hmask;
+                if (filt) {
+                    const uint32_t f = filter_bit(w);
+                    atomicOr(&S[kFilterSlots + (f >> 5)], 1u << (f & 31));
+                }
             }
             __syncwarp();
             if (VM >= 3) vc.on = e1 - e0 < 65536u && hmask < kVtxSlots;   // one counter per hash slot
             PROF_MARK(2);
             PROF_CNT(18);
-            acc = intersect_row<1, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+            if (filt)
+                acc = intersect_row<3, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+            else
+                acc = intersect_row<1, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+            if (filt) {
+                __syncwarp();
+                for (uint32_t k = lane; k < la; k += 32) S[kFilterSlots + (filter_bit(__ldg(A + k)) >> 5)] = 0u;
+            }
             __syncwarp();
             if (VM >= 3 && vc.on) {
                 const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
