@@ -777,6 +777,10 @@ constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
 #define PGABB_LIGHT_PREFETCH 1
 #endif
 constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
+#ifndef PGABB_LIGHT_VPIPE
+#define PGABB_LIGHT_VPIPE 1
+#endif
+constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
 
 // IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
 // wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
@@ -876,9 +880,30 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
         } else {
             const uint64_t rp_jx = T.rp_jx;
             const uint32_t* __restrict__ Bc = col + T.col_jx;
+            // software pipeline (PGABB_LIGHT_VPIPE): the next v and its list bounds are
+            // loaded while the current list is scanned
+            uint32_t vn = 0, bn0 = 0, bn1 = 0;
+            if (kLightVPipe) {
+                vn = __ldg(col + col_ij + e0);
+                bn0 = __ldg(rowptr + rp_jx + vn);
+                bn1 = __ldg(rowptr + rp_jx + vn + 1);
+            }
             for (uint32_t e = e0; e < e1; ++e) {
-                const uint32_t v = __ldg(col + col_ij + e);
-                const uint32_t b0 = __ldg(rowptr + rp_jx + v), b1 = __ldg(rowptr + rp_jx + v + 1);
+                uint32_t v, b0, b1;
+                if (kLightVPipe) {
+                    v = vn;
+                    b0 = bn0;
+                    b1 = bn1;
+                    if (e + 1 < e1) {
+                        vn = __ldg(col + col_ij + e + 1);
+                        bn0 = __ldg(rowptr + rp_jx + vn);
+                        bn1 = __ldg(rowptr + rp_jx + vn + 1);
+                    }
+                } else {
+                    v = __ldg(col + col_ij + e);
+                    b0 = __ldg(rowptr + rp_jx + v);
+                    b1 = __ldg(rowptr + rp_jx + v + 1);
+                }
                 const uint32_t lb = b1 - b0;
                 uint32_t c = 0;
                 if (lb <= kLightScan) {
