@@ -21,3 +21,4 @@ done
 timeout 900 python bench.py --config c5 --budget-gb 12 --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_c5b12$T.json 2> gpurun_out/bench_c5b12$T.err
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench_ws2$T.json 2> gpurun_out/bench_ws2$T.err; echo "ws2 rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref$T.json 2> gpurun_out/ref$T.err; cut -c1-160 gpurun_out/ref$T.json
+timeout 1500 python tools/sim_ranks.py c5 1 2 4 8 --measured > gpurun_out/simm_c5$T.json 2> gpurun_out/simm_c5$T.err; tail -n 1 gpurun_out/simm_c5$T.err
