@@ -95,6 +95,14 @@ constexpr int kDenseUnroll = PGABB_DENSE_UNROLL;   // bit tests in flight per la
 #define PGABB_DENSE_ROW_MUL 16
 #endif
 constexpr uint32_t kDenseRowMul = PGABB_DENSE_ROW_MUL;
+#ifndef PGABB_DENSE_ROW_MUL_WIDE
+#define PGABB_DENSE_ROW_MUL_WIDE 8   // A/B: c5s -5 %, c2 unchanged (its hub part is <= 32 words)
+#endif
+#ifndef PGABB_DENSE_ROW_WIDE_W
+#define PGABB_DENSE_ROW_WIDE_W 32
+#endif
+constexpr uint32_t kDenseRowMulWide = PGABB_DENSE_ROW_MUL_WIDE;   // for parts wider than kDenseRowWideW words
+constexpr uint32_t kDenseRowWideW = PGABB_DENSE_ROW_WIDE_W;
 #ifndef PGABB_ROW_CHUNK
 #define PGABB_ROW_CHUNK 4
 #endif
@@ -621,7 +629,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
         VCnt vc{vcnt, vpre, tvx, false};
         PROF_MARK(0);
-        if (T.bm_jx != ~0ull && 8 * la <= kDenseRowMul * T.bm_words) {
+        if (T.bm_jx != ~0ull && 8 * la <= (T.bm_words > kDenseRowWideW ? kDenseRowMulWide : kDenseRowMul) * T.bm_words) {
             acc = probe_dense_row<VM>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);
