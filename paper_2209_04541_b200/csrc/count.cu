@@ -138,8 +138,16 @@ constexpr uint32_t kPreWords = (kSetWords / kPreGroup + 1) / 2;
 constexpr uint32_t kScratchWordsV = 128 + kPreWords + kVtxSlots / 2;
 // VM (per-vertex roles, NEXT-1): 0 count only; 1 the row's lowest vertex u; 2 + the
 // middle vertex v (per pair); 3 + the highest vertex w (per hit, warp counters)
+// PGABB_VTX_INSET: the per-vertex counters of a bitmap row live in the unused
+// tail of the warp's 4 KB set (a part of W <= kInsetMaxW words leaves 1024 - W
+// words free), so the VM = 3 kernel keeps the counting kernel's footprint and
+// occupancy; hash-set rows then credit w with global atomics.
+#ifndef PGABB_VTX_INSET
+#define PGABB_VTX_INSET 1
+#endif
+constexpr bool kVtxInset = PGABB_VTX_INSET;
 __host__ __device__ constexpr uint32_t scratch_words(int vm) {
-    return vm >= 3 ? kScratchWordsV : vm >= 1 ? 128u : kScratchWords;
+    return vm >= 3 && !kVtxInset ? kScratchWordsV : vm >= 1 ? 128u : kScratchWords;
 }
 
 // Per-vertex counts, third vertex w (NEXT-1): a hub w is hit by many v of the same
@@ -577,10 +585,10 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     const int wid = threadIdx.x >> 5;
     uint32_t* S = smem + wid * (kSetWords + scratch_words(VM));
     uint32_t* scratch = S + kSetWords;
-    uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt)
+    uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt; per row when inset)
     uint32_t* vcnt = vpre + kPreWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
-    if (VM >= 3)
+    if (VM >= 3 && !kVtxInset)
         for (uint32_t k = lane; k < kVtxSlots / 2; k += 32) vcnt[k] = 0;   // invariant: zero between rows
     __syncwarp();
     // Warps claim kRowChunk items at a time from one counter, so the items in
@@ -639,12 +647,18 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 atomicOr(&S[w >> 5], 1u << (w & 31));
             }
             __syncwarp();
-            if (VM >= 3 && la <= kVtxSlots && e1 - e0 < 65536u) {
+            const uint32_t Wx = (T.wx + 31) / 32, NGx = (Wx + kPreGroup - 1) / kPreGroup;
+            if (VM >= 3 && kVtxInset) {   // counters in S's free tail: [Wx, +pre) then cnt
+                vc.pre = S + Wx;
+                vc.cnt = S + Wx + (NGx + 1) / 2;
+            }
+            if (VM >= 3 && la <= kVtxSlots && e1 - e0 < 65536u &&
+                (!kVtxInset || Wx + (NGx + 1) / 2 + (la + 1) / 2 <= kSetWords)) {
                 // prefix popcounts of S per group of kPreGroup words (u16): the rank of a
                 // member w is pre[group] + the popcounts of the words before it in its group
                 vc.on = true;
-                const uint32_t W = (T.wx + 31) / 32, NG = (W + kPreGroup - 1) / kPreGroup;
-                uint16_t* pre16 = reinterpret_cast<uint16_t*>(vpre);
+                const uint32_t W = Wx, NG = NGx;
+                uint16_t* pre16 = reinterpret_cast<uint16_t*>(vc.pre);
                 uint32_t run = 0;
                 for (uint32_t b = 0; b < NG; b += 32) {
                     const uint32_t g = b + lane;
@@ -675,17 +689,21 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             }
             __syncwarp();
             if (VM >= 3 && vc.on) {   // flush the row's w counters: one atomic per distinct w
-                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
+                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vc.cnt);
                 for (uint32_t k = lane; k < la; k += 32) {
                     const uint32_t c = c16[k];
                     if (c) atomicAdd(tvx + __ldg(A + k), (unsigned long long)c);
                 }
                 __syncwarp();
-                for (uint32_t k = lane; k < (la + 1) / 2; k += 32) vcnt[k] = 0u;
+                for (uint32_t k = lane; k < (la + 1) / 2; k += 32) vc.cnt[k] = 0u;
+                if (kVtxInset)   // the prefix words sit inside S, which is all-zero between rows
+                    for (uint32_t k = lane; k < (NGx + 1) / 2; k += 32) vc.pre[k] = 0u;
             }
             for (uint32_t k = lane; k < la; k += 32) S[__ldg(A + k) >> 5] = 0u;
         } else if (mode == 1) {
-            const bool filt = kHashFilter && hmask < kFilterSlots;
+            // (the per-vertex kernel with inset counters uses the set's free tail for
+            // them instead of the filter)
+            const bool filt = kHashFilter && hmask < kFilterSlots && !(VM >= 3 && kVtxInset);
             for (uint32_t k = lane; k < la; k += 32) {
                 const uint32_t w = __ldg(A + k);
                 uint32_t h = hash_slot(w, hbits);
@@ -696,7 +714,14 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
                 }
             }
             __syncwarp();
-            if (VM >= 3) vc.on = e1 - e0 < 65536u && hmask < kVtxSlots;   // one counter per hash slot
+            if (VM >= 3) {   // one u16 counter per hash slot
+                if (kVtxInset) {
+                    vc.cnt = S + hmask + 1;
+                    vc.on = e1 - e0 < 65536u && (hmask + 1) + (hmask + 1) / 2 <= kSetWords;
+                } else {
+                    vc.on = e1 - e0 < 65536u && hmask < kVtxSlots;
+                }
+            }
             PROF_MARK(2);
             PROF_CNT(18);
             if (filt)
@@ -709,13 +734,13 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             }
             __syncwarp();
             if (VM >= 3 && vc.on) {
-                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vcnt);
+                const uint16_t* c16 = reinterpret_cast<const uint16_t*>(vc.cnt);
                 for (uint32_t k = lane; k <= hmask; k += 32) {
                     const uint32_t c = c16[k];
                     if (c) atomicAdd(tvx + (S[k] - 1u), (unsigned long long)c);
                 }
                 __syncwarp();
-                for (uint32_t k = lane; k < (hmask + 1) / 2; k += 32) vcnt[k] = 0u;
+                for (uint32_t k = lane; k < (hmask + 1) / 2; k += 32) vc.cnt[k] = 0u;
             }
             for (uint32_t k = lane; k <= hmask; k += 32) S[k] = 0u;
         } else {
