@@ -117,7 +117,10 @@ __device__ __forceinline__ unsigned long long claim_items(unsigned long long* ne
     end = b + kRowChunk < n ? b + kRowChunk : n;
     return b;
 }
-constexpr int kRowMinBlocks = 5;   // = the shared-memory limit (5 x 8 warps x 4.4 KB)
+#ifndef PGABB_ROW_MINB
+#define PGABB_ROW_MINB 5
+#endif
+constexpr int kRowMinBlocks = PGABB_ROW_MINB;   // CTAs per SM (5 x 8 warps x 4.4 KB of sets; 48 registers)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
 constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
 // per-vertex kernel: + the batch's v ids (32), the row's prefix popcounts of S
