@@ -21,6 +21,10 @@
  *                         handles), S10 the intersections
  *                         n_t += |A_ix[u] ∩ A_jx[v]| for every (u,v) in A_ij
  *                         (Listing 5), S11 the count reduction.
+ *   Beyond the count: pgabb_vertex_triangles / pgabb_local_clustering
+ *   (per-vertex t(v), NEXT-1), pgabb_connected_components (Shiloach-Vishkin on the
+ *   same blocks, NEXT-4), pgabb_task_times (measured task estimates for S8), and
+ *   host-resident streaming through a device budget (S9 / NEXT-2, build options).
  *
  * Conventions (all entry points):
  *   - No C++ types or exceptions cross this boundary.  Every function returns a
