@@ -132,6 +132,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    """The host CPU the oracle ran on (/proc/cpuinfo model name)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(cfg_name, n, s, d, target_s):
     """The oracle (oracle/tc_oracle.c) as it stands, on this host's cores, over a
     bounded vertex-stride sample of the same graph (full graph when it fits)."""
@@ -153,7 +165,7 @@ def cpu_baseline(cfg_name, n, s, d, target_s):
     g.close()
     sample = ("full graph" if stride == 1 else
               f"every {stride}-th vertex as the lowest triangle vertex ({e_s} of {m_edges} DAG edges)")
-    return {"value": e_s / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+    return {"value": e_s / dt, "unit": UNIT, "cores": oracle.threads(), "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{cfg_name}: node iterator over {sample}; oracle build {t_build:.1f}s excluded",
             "seconds": dt, "triangles_in_sample": T_s, "full": stride == 1}
 
@@ -192,7 +204,8 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "m_edges": m_edges,
                    "sample_stride": stride, "device": "host CPU (the oracle; no GPU used)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "cpu_model": cpu_model(),
+                         "kind": "oracle",
                          "sample": f"each step: node iterator over every {stride}-th vertex (rotating offset)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
