@@ -30,13 +30,16 @@ METRIC = "triangle-count edges/sec (|E|/time)"
 UNIT = "edges/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="GPUs (= ranks, one process per GPU).  Without WORLD_SIZE in the environment "
+                         "bench.py relaunches itself under torch.distributed.run with N ranks")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5",
+                    help="c5 (Graph500 R-MAT s26 ef32, the headline) | c2 | c3 | c4 | c1 | c5s")
     ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
     ap.add_argument("--cut-rule", type=int, default=0)
     ap.add_argument("--path", choices=["count", "vertex", "vertex2", "cc"], default="count",
@@ -48,10 +51,30 @@ def parse():
     ap.add_argument("--budget-gb", type=float, default=0.0,
                     help="> 0: blocks stay in pinned host memory and each count streams them through "
                          "a device budget of this many GB (S9 out-of-core mode, PAPER.md:829-835)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="flow tests only: allow more ranks than visible GPUs (ranks share a GPU, gloo)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def self_launch(args):
+    """--gpus N without a torchrun environment: check that N GPUs are visible and
+    re-run this script as N ranks (one process per GPU) under torch.distributed.run."""
+    import socket
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < args.gpus and not args.shared_gpu:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {ndev} CUDA device(s) visible"}),
+              flush=True)
+        sys.exit(1)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_env():
@@ -71,16 +94,39 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(config, kernel):
-    """DRAM bytes (read + write) per launch of `kernel` on `config` from the committed
-    ncu --set full summary (profiles/ncu_summary.json, written by tools/make_profile.py)."""
+NOMINAL_HBM_GBS = 8000.0   # the north star's ~8 TB/s nominal B200 HBM3e figure (the stricter denominator)
+KERNEL_SOURCES = ("paper_2209_04541_b200/csrc/count.cu", "paper_2209_04541_b200/csrc/internal.h")
+
+
+def kernel_src_hash():
+    """sha256 (12 hex) of the S10 kernel sources: an ncu summary is current only for this hash."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        with open(os.path.join(ROOT, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:12]
+
+
+def ncu_entry(config, kernel):
+    """The committed ncu capture of `kernel` on `config` (profiles/ncu_summary.json,
+    written by tools/make_profile.py from an `ncu --set full` / counter capture of this
+    command on a B200): DRAM bytes per launch, issue activity, warp instructions."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            js = json.load(f)
-        return js.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
+            e = json.load(f).get(config, {}).get(kernel)
     except Exception:
         return None
+    if e is not None:
+        e = dict(e)
+        e["current"] = e.get("src_hash") == kernel_src_hash()
+    return e
+
+
+def stats_of(xs):
+    xs = sorted(xs)
+    return {"median": statistics.median(xs), "min": xs[0], "max": xs[-1], "mean": statistics.mean(xs)}
 
 
 class ClockSampler:
@@ -170,6 +216,15 @@ def cpu_baseline(cfg_name, n, s, d, target_s):
             "seconds": dt, "triangles_in_sample": T_s, "full": stride == 1}
 
 
+L2_NOTE = "L2 flushed (256 MiB write) between timed steps, outside the events"
+
+
+def workload_config(cfg, args, n, m_tuples, m_edges, p):
+    """The workload keys, identical in both arms (ours and --impl reference)."""
+    return {"workload": f"{cfg.name}: {cfg.desc}", "path": args.path, "n": n, "tuples": m_tuples,
+            "m_edges": m_edges, "p": p, "cut_rule": args.cut_rule, "l2": L2_NOTE}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -187,23 +242,26 @@ def run_reference(args):
     t_probe = max(time.perf_counter() - t0, 1e-4)
     per_step = max(1.0, 60.0 / max(args.steps + args.warmup, 1))   # whole run ~1 min
     stride = max(1, int(t_probe * 256 / per_step + 0.999))
-    times, edges = [], []
+    rates, times = [], []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         _, e = g.count_range(k % stride, n, stride)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
-            edges.append(e)
+            rates.append(e / dt)
     g.close()
-    value = sum(edges) / sum(times)
+    value = statistics.median(rates)
+    p = max(1, min(args.p or cfg.p, n))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(ws, args.gpus),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.desc}", "m_edges": m_edges,
-                   "sample_stride": stride, "device": "host CPU (the oracle; no GPU used)"},
+        "config": workload_config(cfg, args, n, int(s.size), m_edges, p),
+        "run": {"device": "host CPU (the oracle, oracle/tc_oracle.c; no GPU used)", "sample_stride": stride,
+                "step": f"node iterator over every {stride}-th vertex as the lowest triangle vertex "
+                        "(rotating offset); value = median over steps of sampled DAG edges / step time"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "cpu_model": cpu_model(),
                          "kind": "oracle",
                          "sample": f"each step: node iterator over every {stride}-th vertex (rotating offset)"},
@@ -214,15 +272,18 @@ def run_reference(args):
 
 
 class Comm:
-    """Process-group plumbing for N>1: NCCL when every rank has its own GPU (the
-    production path: the 8-byte count allreduce runs on the GPU stream); gloo with
-    host tensors when ranks share a GPU (lets the multi-rank flow run on a 1-GPU box)."""
+    """Process-group plumbing for N>1: NCCL, one rank per GPU (the production path:
+    the 8-byte count allreduce runs on the GPU stream).  With --shared-gpu (flow
+    tests on a 1-GPU box only) ranks share a GPU and talk gloo with host tensors."""
 
-    def __init__(self, ws, local):
+    def __init__(self, ws, local, shared_ok=False):
         import torch
         import torch.distributed as dist
         self.ws, self.dist, self.torch = ws, dist, torch
         ndev = torch.cuda.device_count()
+        if ws > ndev and not shared_ok:
+            raise SystemExit(f"bench.py: {ws} ranks but {ndev} CUDA device(s) visible "
+                             "(one process per GPU; --shared-gpu only for flow tests)")
         self.dev = local % max(ndev, 1)
         torch.cuda.set_device(self.dev)
         self.backend = None
@@ -263,6 +324,56 @@ def golden_triangles(config):
         return None
 
 
+def roofline_of(cfg_name, kernels, ms_step, peak, peak_src, vertex, sm_clock_mhz, sms):
+    """roofline of the dominant S10 kernel.
+
+    achieved/frac: LOGICAL bytes (the R19 staged-list model) per launch
+    / the kernel's live CUDA-event time -- the metric's "% of HBM roofline".  Hub
+    lists are re-read from L2, so this is an effective bandwidth that can exceed 1.
+    What actually limits the kernel comes from the committed ncu capture of this
+    config (DRAM bytes, issue activity): `bound` is "hbm" when DRAM is the busier
+    unit, "alu" when instruction issue is."""
+    dom = max(kernels, key=lambda k: k["ms"])
+    nc = ncu_entry(cfg_name, dom["kernel"]) if not vertex else None
+    r = {"bound": "hbm", "achieved": dom["achieved"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
+         "traffic": None, "achieved_kind": "logical_bytes (R19 staged-list model; L2-served re-reads count)",
+         "frac_nominal_8tbs": dom["achieved"] / NOMINAL_HBM_GBS, "peak_source": peak_src,
+         "kernel": dom["kernel"] + ("<VTX> (S10 + t(v) atomics)" if vertex else " (S10 intersections)"),
+         "kernel_ms": dom["ms"], "kernel_share_of_step": dom["ms"] / ms_step if ms_step else None,
+         "alg_bytes_per_launch": dom["alg_bytes"], "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19",
+         "kernels": kernels}
+    if nc:
+        dram = nc.get("dram_bytes_per_launch")
+        r["traffic"] = dram
+        r["ncu"] = {k: nc.get(k) for k in ("source", "src_hash", "current", "l2_hit_pct", "issue_active_pct",
+                                           "warp_inst_per_launch", "top_stall", "kernel_ms_under_ncu")}
+        dfrac = ifrac = None
+        if dram is not None and dom["ms"] > 0:
+            dgbs = dram / (dom["ms"] / 1e3) / 1e9
+            dfrac = dgbs / peak
+            r["dram_gbs"] = dgbs
+            r["dram_frac"] = dfrac
+            r["dram_frac_nominal_8tbs"] = dgbs / NOMINAL_HBM_GBS
+        inst = nc.get("warp_inst_per_launch")
+        if inst and dom["ms"] > 0 and sm_clock_mhz:
+            # issue roofline: one warp instruction per SMSP per cycle, 4 SMSPs per SM
+            ipeak = 4.0 * sms * sm_clock_mhz * 1e6
+            ach = inst / (dom["ms"] / 1e3)
+            ifrac = ach / ipeak
+            r["issue"] = {"achieved": ach, "peak": ipeak, "unit": "warp-inst/s", "frac": ifrac,
+                          "peak_basis": f"4 SMSP x {sms} SMs x {sm_clock_mhz:.0f} MHz (measured clock)",
+                          "inst_per_logical_elem": inst / max(1.0, dom["alg_bytes"] / 4.0)}
+        if dfrac is not None and ifrac is not None:
+            r["bound"] = "hbm" if dfrac >= ifrac else "alu"
+            top = nc.get("top_stall") or ""
+            if max(dfrac, ifrac) < 0.6 and "long_scoreboard" in top:
+                r["limiter"] = (f"memory latency (top stall {top}; issue {ifrac:.2f}, DRAM {dfrac:.2f} of peak)")
+            else:
+                r["limiter"] = ("HBM bandwidth" if r["bound"] == "hbm" else "instruction issue") + \
+                               f" (issue {ifrac:.2f}, DRAM {dfrac:.2f} of peak)"
+    return r
+
+
 def run_ours(args):
     import torch
 
@@ -270,7 +381,9 @@ def run_ours(args):
     import paper_2209_04541_b200 as pg
 
     ws, rank, local = dist_env()
-    comm = Comm(ws, local)
+    if ws > 1 and args.gpus not in (1, ws):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    comm = Comm(ws, local, args.shared_gpu)
     dev = comm.dev
     cfg = CONFIGS[args.config]
     p = args.p or cfg.p
@@ -313,7 +426,7 @@ def run_ours(args):
             b.vertex_triangles(stream=stream, out=tv_dev, sync=False)
             comm.allreduce_(tv_dev)
             return
-        b.triangle_count(stream=stream.cuda_stream, d_count=out.data_ptr(), sync=False)
+        b.triangle_count(stream=stream, d_count=out.data_ptr(), sync=False)
         comm.allreduce_(out)            # S11: one 8-byte allreduce of the per-rank counts
 
     for _ in range(args.warmup):
@@ -344,16 +457,17 @@ def run_ours(args):
         torch.cuda.synchronize()
         comm.barrier()
     step_ms = [a.elapsed_time(z) for a, z in ev]
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    # per-rank step time (balance evidence): rank r's slot, summed over ranks
+    # every step's time is the max over ranks (the slowest rank ends the step); the
+    # reported step time is the median over steps (median of runs)
+    per_step = torch.tensor(step_ms, dtype=torch.float64, device="cuda")
+    per_step_max = [float(x) for x in comm.allreduce_(per_step, "max").cpu()]
     per_rank = torch.zeros(ws, dtype=torch.float64, device="cuda")
-    per_rank[rank] = sum(step_ms) / args.steps
+    per_rank[rank] = statistics.median(step_ms)
     per_rank_ms = [float(x) for x in comm.allreduce_(per_rank).cpu()]
-    tot_ms = float(comm.allreduce_(tot, "max").item())       # max over ranks
-    ms_per_step = tot_ms / args.steps
+    sstat = stats_of(per_step_max)
+    ms_per_step = sstat["median"]
     value = m_edges / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel (the intersection kernel, S10)
     peak, peak_src = load_peaks()
     st = b.stats()
     alg = int(st["alg_bytes_local"])
@@ -362,8 +476,8 @@ def run_ours(args):
         alg += 3 * 8 * n
     if b_rev is not None:   # the reversed pass streams its own staged-model bytes
         alg += int(b_rev.stats()["alg_bytes_local"]) + 3 * 8 * n
-    kms = statistics.mean(kern_ms) if kern_ms else float("nan")
-    lms = statistics.mean(light_ms) if light_ms else 0.0
+    kms = statistics.median(kern_ms) if kern_ms else float("nan")
+    lms = statistics.median(light_ms) if light_ms else 0.0
     alg_l = int(st["alg_bytes_light"]) + (int(b_rev.stats()["alg_bytes_light"]) if b_rev is not None else 0)
 
     def kern(name, ms, nbytes):
@@ -371,22 +485,18 @@ def run_ours(args):
         return {"kernel": name, "ms": ms, "alg_bytes": nbytes, "achieved": ach, "frac": ach / peak}
     # S10 runs as two kernels (DESIGN R20): warp-per-row k_tc_rows, thread-per-row k_tc_light
     kernels = [kern("k_tc_rows", kms - lms, alg - alg_l), kern("k_tc_light", lms, alg_l)]
-    dom = max(kernels, key=lambda k: k["ms"])
-    both = kern("k_tc_rows + k_tc_light", kms, alg)
-    roofline = {"bound": "hbm", "achieved": dom["achieved"], "peak": peak, "unit": "GB/s",
-                "frac": dom["frac"], "traffic": load_traffic(args.config, dom["kernel"]) if ws == 1 else None,
-                "kernel": dom["kernel"] + ("<VTX> (S10 + t(v) atomics)" if vertex else " (S10 intersections)"),
-                "kernel_ms": dom["ms"], "kernel_share_of_step": dom["ms"] / ms_per_step if ms_per_step else None,
-                "alg_bytes_per_launch": dom["alg_bytes"], "peak_source": peak_src,
-                "model": "staged-list bytes, SURVEY 8(d) / DESIGN R19",
-                "kernels": kernels, "s10_combined": both,
-                "items": {"heavy": int(st["items_heavy"]), "light": int(st["items_light"])}}
+    clocks = clk.summary()
+    roofline = roofline_of(args.config, kernels, ms_per_step, peak, peak_src, vertex,
+                           clocks.get("sm_mhz") or 1965.0, torch.cuda.get_device_properties(dev).multi_processor_count)
+    roofline["s10_combined"] = kern("k_tc_rows + k_tc_light", kms, alg)
+    roofline["items"] = {"heavy": int(st["items_heavy"]), "light": int(st["items_light"])}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
     if not args.no_e2e and not vertex and args.budget_gb <= 0:
         bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
-                             residency=pg.RESIDENT_HOST)
+                             residency=pg.RESIDENT_HOST,
+                             task_weights=getattr(b, "task_weights_used", None))
         for _ in range(max(1, args.warmup)):
             bh.triangle_count()
         comm.barrier()
@@ -401,12 +511,13 @@ def run_ours(args):
             comm.allreduce_(tt)
             tt.item()
             wall.append(time.perf_counter() - t0)
-        e_t = torch.tensor([sum(wall)], dtype=torch.float64, device="cuda")
-        e_s = float(comm.allreduce_(e_t, "max").item())
+        e_t = torch.tensor(wall, dtype=torch.float64, device="cuda")
+        e_s = statistics.median(float(x) for x in comm.allreduce_(e_t, "max").cpu())
         sh = bh.stats()
-        e2e = {"value": m_edges / (e_s / args.steps), "unit": UNIT,
+        e2e = {"value": m_edges / e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(sh["h2d_bytes_last"]), "d2h_bytes_per_step": 8,
-               "ms_per_step": 1e3 * e_s / args.steps, "timer": "host wall clock around the public call"}
+               "ms_per_step": 1e3 * e_s, "timer": "host wall clock around the public call, median of steps, "
+                                                 "max over ranks"}
         bh.free()
 
     cpu = None
@@ -418,24 +529,23 @@ def run_ours(args):
             "metric": METRIC if not vertex else "per-vertex triangle-count edges/sec (|E|/time)",
             "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.desc}", "path": args.path, "n": n, "tuples": m_tuples, "m_edges": m_edges,
-                       "p": int(st["p"]), "cut_rule": args.cut_rule, "tasks": int(st["ntasks"]),
-                       "triangles": T, "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
-                       "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}", "balance": args.balance if ws > 1 else None,
-                       "per_rank_ms": per_rank_ms,
-                       "comm": comm.backend,
-                       "residency": (f"host-streamed through a {args.budget_gb:g} GB device budget, "
-                                     f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B + D2D reuse "
-                                     f"{int(st['d2d_bytes_last'])} B per count "
-                                     "inside the timed region") if args.budget_gb > 0 else "device",
-                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                       "timer": "CUDA events per step on the launch stream, max over ranks"},
+            "scaling": "weak" if ws > 1 else "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": workload_config(cfg, args, n, m_tuples, m_edges, int(st["p"])),
+            "run": {"step_ms": sstat, "per_rank_ms": per_rank_ms, "triangles": T, "tasks": int(st["ntasks"]),
+                    "wedges": int(st["wedges"]), "alg_bytes": int(st["alg_bytes_total"]),
+                    "build_ms": float(st0["ms_build"]), "parallelism": f"task-parallel x{ws}",
+                    "balance": args.balance if ws > 1 else None, "comm": comm.backend,
+                    "residency": (f"host-streamed through a {args.budget_gb:g} GB device budget, "
+                                  f"{int(st['waves'])} waves, H2D {int(st['h2d_bytes_last'])} B + D2D reuse "
+                                  f"{int(st['d2d_bytes_last'])} B per count "
+                                  "inside the timed region") if args.budget_gb > 0 else "device",
+                    "timer": "CUDA events per step on the launch stream; per step the max over ranks; "
+                             "value from the median step"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if vertex:
             line["vertex_route"] = ("two-pass (low+mid forward, low reversed; R24)" if b_rev is not None
@@ -526,6 +636,8 @@ def run_cc(args):
 
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.path == "cc":

@@ -79,7 +79,9 @@ typedef struct {
     uint32_t cut_rule;          /* 0 = balance estimated work w(v) = d+(v) + d-(v)d+(v)
                                    1 = balance DAG out-degree w(v) = d+(v)   (DESIGN R7) */
     int32_t device;             /* CUDA ordinal, -1 = current device */
-    uint32_t inputs_on_device;  /* 1: src/dst are device pointers on `device` */
+    uint32_t inputs_on_device;  /* 1: src/dst are device pointers on `device`; the build
+                                   synchronizes the device before reading them, so tuples
+                                   still being produced on any stream are complete */
     int32_t rank;               /* this handle's rank in [0, world_size) (S8) */
     int32_t world_size;         /* ranks sharing the tasks; <= 1 means one GPU */
     uint32_t residency;         /* PGABB_RESIDENT_DEVICE or PGABB_RESIDENT_HOST */
@@ -119,7 +121,12 @@ PGABB_API pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32
                                   pgabb_blocks_t* out);
 
 typedef struct {
-    void* cuda_stream;          /* cudaStream_t to order the work on; NULL = handle's stream */
+    void* cuda_stream;          /* cudaStream_t to order the work on; NULL = handle's stream.
+                                   The legacy default stream is cudaStreamLegacy ((void*)1),
+                                   NOT NULL.  Calls on one handle are serialized on the
+                                   device across streams: each call first waits for the
+                                   previous call's work (a per-handle event), because they
+                                   share the handle's scratch (task counts, arenas, t(v)). */
     uint64_t* d_count;          /* optional DEVICE uint64*: receives this rank's count,
                                    stream-ordered (for a caller-side NCCL allreduce) */
     uint64_t* task_counts;      /* optional HOST uint64[ntasks]: per-task counts of the

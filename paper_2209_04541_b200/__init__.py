@@ -41,6 +41,18 @@ def version() -> str:
     return _lib.pgabb_version().decode()
 
 
+_CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the ABI reads NULL as "the handle's own stream"
+
+
+def _stream_arg(stream):
+    """cudaStream_t for CountOpts.cuda_stream from a torch stream or a raw handle.
+    torch's default stream reports cuda_stream == 0 (the legacy default stream);
+    passed through as NULL the library would use its private non-blocking stream,
+    unordered with torch's work, so 0 becomes cudaStreamLegacy."""
+    raw = int(getattr(stream, "cuda_stream", stream) or 0)
+    return raw if raw else _CUDA_STREAM_LEGACY
+
+
 def _pointer(x):
     """(pointer, length, on_device, keepalive) for a numpy array or torch tensor of uint32/int32."""
     if hasattr(x, "data_ptr") and hasattr(x, "is_cuda"):
@@ -53,6 +65,12 @@ def _pointer(x):
         x = x.numpy()
     a = np.ascontiguousarray(x)
     if a.dtype not in (np.uint32, np.int32):
+        if a.dtype.kind not in "iu":
+            raise TypeError(f"tuples must be integers, got {a.dtype}")
+        # a wider integer array is narrowed only when every id fits in uint32 (ids of
+        # 2^32 or more would otherwise wrap to small ids and count another graph)
+        if a.size and (int(a.min()) < 0 or int(a.max()) >= (1 << 32)):
+            raise ValueError("vertex ids must lie in [0, 2^32)")
         a = a.astype(np.uint32)
     return a.ctypes.data, a.size, False, a
 
@@ -91,7 +109,7 @@ class Blocks:
         return the per-task counts."""
         o = _abi.CountOpts()
         if stream is not None:
-            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+            o.cuda_stream = _stream_arg(stream)
         if d_count is not None:
             o.d_count = d_count
         tc = np.zeros(max(self.ntasks, 1), np.uint64) if task_counts else None
@@ -116,7 +134,7 @@ class Blocks:
         o = _abi.CountOpts()
         o.flags = {"all": 0, "low": _abi.ROLE_LOW, "low+mid": _abi.ROLE_LOW | _abi.ROLE_MID}[roles]
         if stream is not None:
-            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+            o.cuda_stream = _stream_arg(stream)
         cnt = ctypes.c_uint64(0)
         if out is not None:
             if not getattr(out, "is_cuda", False) or out.numel() < self.n or out.element_size() != 8:
@@ -135,7 +153,7 @@ class Blocks:
         numpy float64 out, or a CUDA 8-byte tensor in -> CUDA float64 tensor out."""
         o = _abi.CountOpts()
         if stream is not None:
-            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+            o.cuda_stream = _stream_arg(stream)
         if getattr(tv, "is_cuda", False):
             import torch
             if tv.numel() < self.n or tv.element_size() != 8:
@@ -160,7 +178,7 @@ class Blocks:
         written into ``out``, a CUDA 4-byte tensor of n entries)."""
         o = _abi.CountOpts()
         if stream is not None:
-            o.cuda_stream = getattr(stream, "cuda_stream", stream)
+            o.cuda_stream = _stream_arg(stream)
         nc, it = ctypes.c_uint64(0), ctypes.c_uint32(0)
         if out is not None:
             if not getattr(out, "is_cuda", False) or out.numel() < self.n or out.element_size() != 4:

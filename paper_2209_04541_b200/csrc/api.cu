@@ -80,7 +80,7 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_deg.release();
     d_tv_rank.release();
     h_result.release();
-    for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_mid})
+    for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_mid, ev_last})
         if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (prev >= 0) cudaSetDevice(prev);
@@ -129,6 +129,7 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->device = dev;
         PG_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&h->ev0, &h->ev1, &h->ev2, &h->ev3, &h->ev_mid}) PG_CK(cudaEventCreate(e));
+        PG_CK(cudaEventCreateWithFlags(&h->ev_last, cudaEventDisableTiming));
         h->h_result.alloc(1);
         h->n = n;
         h->m_tuples = m;
@@ -159,12 +160,12 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         if (h->residency == PGABB_RESIDENT_HOST) {
             h->h_col.alloc(h->d_col.n);
             h->h_rowptr.alloc(h->d_rowptr.n);
-            if (h->d_col.n) PG_CK(cudaMemcpy(h->h_col.p, h->d_col.p, h->d_col.bytes(), cudaMemcpyDeviceToHost));
+            if (h->d_col.n) PG_COPY_SYNC(h->h_col.p, h->d_col.p, h->d_col.bytes(), h->stream);
             if (h->d_rowptr.n)
-                PG_CK(cudaMemcpy(h->h_rowptr.p, h->d_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyDeviceToHost));
+                PG_COPY_SYNC(h->h_rowptr.p, h->d_rowptr.p, h->d_rowptr.bytes(), h->stream);
             h->h_bitmap.alloc(h->d_bitmap.n);
             if (h->d_bitmap.n)
-                PG_CK(cudaMemcpy(h->h_bitmap.p, h->d_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyDeviceToHost));
+                PG_COPY_SYNC(h->h_bitmap.p, h->d_bitmap.p, h->d_bitmap.bytes(), h->stream);
             if (h->streaming) {   // the graph now lives in pinned host DRAM only
                 h->d_col.release();
                 h->d_rowptr.release();
@@ -295,7 +296,7 @@ pgabb_status_t pgabb_get_rank(pgabb_blocks_t b, uint32_t* rank) {
     return guarded([&] {
         if (!b || !rank) fail(PGABB_EINVAL, "NULL argument");
         DeviceGuard g(b->device);
-        if (b->n) PG_CK(cudaMemcpy(rank, b->d_rank.p, (size_t)b->n * 4, cudaMemcpyDeviceToHost));
+        if (b->n) PG_COPY_SYNC(rank, b->d_rank.p, (size_t)b->n * 4, b->stream);
     });
 }
 
@@ -319,11 +320,11 @@ pgabb_status_t pgabb_get_block(pgabb_blocks_t b, uint32_t i, uint32_t j, uint32_
         const uint32_t* col_pool = b->d_col.p ? b->d_col.p : b->h_col.p;
         if (rowptr) {
             if (bi.present)
-                PG_CK(cudaMemcpy(rowptr, rp_pool + bi.rp_off, ((size_t)bi.nrows + 1) * 4, cudaMemcpyDefault));
+                PG_COPY_SYNC(rowptr, rp_pool + bi.rp_off, ((size_t)bi.nrows + 1) * 4, b->stream);
             else
                 std::memset(rowptr, 0, ((size_t)bi.nrows + 1) * 4);
         }
-        if (col && bi.nnz) PG_CK(cudaMemcpy(col, col_pool + bi.col_off, bi.nnz * 4, cudaMemcpyDefault));
+        if (col && bi.nnz) PG_COPY_SYNC(col, col_pool + bi.col_off, bi.nnz * 4, b->stream);
     });
 }
 

@@ -420,6 +420,10 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
     // ---- upload + validate --------------------------------------------------
     DBuf<uint32_t> d_s, d_d;
     const uint32_t *s = src, *d = dst;
+    // device tuples may still be in flight on the caller's streams (a producer
+    // kernel, a copy): the build reads them on the handle's non-blocking stream,
+    // which no caller stream orders against, so wait for all device work first
+    if (on_device) PG_CK(cudaDeviceSynchronize());
     if (!on_device) {
         d_s.alloc(m);
         d_d.alloc(m);
@@ -461,7 +465,7 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
     uint64_t mE = nuniq;
     if (mE) {
         uint64_t last = 0;
-        PG_CK(cudaMemcpy(&last, keys.p + (mE - 1), 8, cudaMemcpyDeviceToHost));
+        PG_COPY_SYNC(&last, keys.p + (mE - 1), 8, st);
         if (last == sent) --mE;
     }
     if (mE >= (1ull << 32)) fail(PGABB_ERANGE, "|E| >= 2^32 is not supported");
@@ -877,16 +881,15 @@ void plan_waves(pgabb_blocks_s* h) {
     close_wave();
     h->d_wave_pieces.alloc(std::max<size_t>(wpieces.size(), 1));
     if (!wpieces.empty())
-        PG_CK(cudaMemcpy(h->d_wave_pieces.p, wpieces.data(), wpieces.size() * sizeof(WavePiece),
-                         cudaMemcpyHostToDevice));
+        PG_COPY_SYNC(h->d_wave_pieces.p, wpieces.data(), wpieces.size() * sizeof(WavePiece), h->stream);
     h->d_wave_tasks.alloc(std::max<size_t>(wtasks.size(), 1));
     if (!wtasks.empty())
-        PG_CK(cudaMemcpy(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
+        PG_COPY_SYNC(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), h->stream);
     uint64_t maxw = 1;
     for (const Wave& wv : h->waves) maxw = std::max(maxw, wv.words);
     for (int a = 0; a < 2; ++a) {   // padded like the col pool (16-byte list covers)
         h->d_arena[a].alloc(maxw + kColPad);
-        PG_CK(cudaMemset(h->d_arena[a].p + maxw, 0, kColPad * 4));
+        PG_CK(cudaMemsetAsync(h->d_arena[a].p + maxw, 0, kColPad * 4, h->stream));
     }
 }
 
@@ -905,8 +908,8 @@ void upload_work(pgabb_blocks_s* h) {
         const BlockInfo &bij = h->blocks[T.i * p + T.j], &bix = h->blocks[T.i * p + T.x],
                         &bjx = h->blocks[T.j * p + T.x];
         uint32_t e0 = 0, e1 = 0;
-        PG_CK(cudaMemcpy(&e0, h->d_rowptr.p + bij.rp_off + pc.r0, 4, cudaMemcpyDeviceToHost));
-        PG_CK(cudaMemcpy(&e1, h->d_rowptr.p + bij.rp_off + pc.r1, 4, cudaMemcpyDeviceToHost));
+        PG_COPY_SYNC(&e0, h->d_rowptr.p + bij.rp_off + pc.r0, 4, h->stream);
+        PG_COPY_SYNC(&e1, h->d_rowptr.p + bij.rp_off + pc.r1, 4, h->stream);
         if (e1 == e0) continue;
         PieceDev w{};
         w.gstart = h->work_edges;
@@ -932,9 +935,41 @@ void upload_work(pgabb_blocks_s* h) {
     }
     h->d_work.alloc(std::max<size_t>(h->work.size(), 1));
     if (!h->work.empty())
-        PG_CK(cudaMemcpy(h->d_work.p, h->work.data(), h->work.size() * sizeof(PieceDev), cudaMemcpyHostToDevice));
+        PG_COPY_SYNC(h->d_work.p, h->work.data(), h->work.size() * sizeof(PieceDev), h->stream);
     h->d_task_counts.alloc(h->tasks.size() + 1);
     h->d_next.alloc(8);
+
+    // S9 (host-resident, no budget): the pool ranges of the blocks the owned pieces read
+    {
+        std::vector<char> need((size_t)p * p, 0);
+        for (const PieceDev& w : h->work) {
+            const Task& T = h->tasks[w.task];
+            need[T.i * p + T.j] = need[T.i * p + T.x] = 1;
+            need[T.j * p + T.x] |= 2;   // bit 1: the v-side block (its dense copy is read too)
+        }
+        std::vector<StagedBlock> r;
+        for (uint32_t b = 0; b < p * p; ++b) {
+            if (!need[b]) continue;
+            const BlockInfo& B = h->blocks[b];
+            if (B.nnz) r.push_back(StagedBlock{B.col_off, B.col_off, B.nnz, 0});
+            if (B.present) r.push_back(StagedBlock{B.rp_off, B.rp_off, (uint64_t)B.nrows + 1, 1});
+            if ((need[b] & 2) && B.bm_off != ~0ull)
+                r.push_back(StagedBlock{B.bm_off, B.bm_off, (uint64_t)B.nrows * B.bm_words, 2});
+        }
+        std::sort(r.begin(), r.end(), [](const StagedBlock& a, const StagedBlock& b) {
+            return a.pool != b.pool ? a.pool < b.pool : a.src_word < b.src_word;
+        });
+        h->host_copies.clear();
+        for (const StagedBlock& c : r) {   // merge adjacent ranges of one pool
+            if (!h->host_copies.empty() && h->host_copies.back().pool == c.pool &&
+                h->host_copies.back().src_word + h->host_copies.back().words == c.src_word)
+                h->host_copies.back().words += c.words;
+            else
+                h->host_copies.push_back(c);
+        }
+        // (cover reads past a copied list stay inside the device pool, whose zero
+        // padding the build wrote, and their ids are masked by the list bounds)
+    }
 
     // task descriptors for the intersection kernel
     std::vector<TaskDev> td(std::max<size_t>(h->tasks.size(), 1));
@@ -953,7 +988,7 @@ void upload_work(pgabb_blocks_s* h) {
         td[t] = d;
     }
     h->d_tasks.alloc(td.size());
-    PG_CK(cudaMemcpy(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), cudaMemcpyHostToDevice));
+    PG_COPY_SYNC(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), h->stream);
 
     // largest block-triple footprint (what one task needs resident, S9)
     h->max_task_bytes = 0;
@@ -1025,7 +1060,7 @@ void upload_work(pgabb_blocks_s* h) {
     h->n_items = nitems;
     h->n_light = nlight;
     unsigned long long alg_light = 0;
-    PG_CK(cudaMemcpy(&alg_light, d_alg.p, 8, cudaMemcpyDeviceToHost));
+    PG_COPY_SYNC(&alg_light, d_alg.p, 8, st);
     h->alg_light = alg_light;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
     h->d_light.alloc(std::max<uint64_t>(nlight, 1));

@@ -150,7 +150,9 @@ __global__ void k_cc_labels(const uint32_t* __restrict__ rank, const uint32_t* _
     if ((threadIdx.x & 31) == 0 && roots) atomicAdd(ncomp, (unsigned long long)roots);
 }
 
-unsigned grid1(uint64_t n) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)); }
+unsigned grid1(uint64_t n, int dev) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(dev) * 16));
+}
 
 }  // namespace
 
@@ -161,6 +163,8 @@ void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uin
     cudaStream_t st = (opts && opts->cuda_stream) ? (cudaStream_t)opts->cuda_stream : h->stream;
     const bool on_dev = opts && (opts->flags & PGABB_OUT_DEVICE);
     const uint32_t n = h->n, p = h->p;
+    settle_timing(h);   // ev0/ev3 are re-recorded below
+    begin_call(h, st);
     if (h->residency == PGABB_RESIDENT_HOST && h->d_col.n) {   // S9: blocks in for this call
         PG_CK(cudaMemcpyAsync(h->d_col.p, h->h_col.p, h->d_col.bytes(), cudaMemcpyHostToDevice, st));
         PG_CK(cudaMemcpyAsync(h->d_rowptr.p, h->h_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyHostToDevice, st));
@@ -198,7 +202,7 @@ void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uin
     PG_CK(cudaEventRecord(h->ev0, st));
     uint32_t it = 0;
     if (n) {
-        k_cc_init<<<grid1(n), 256, 0, st>>>(C.p, n);
+        k_cc_init<<<grid1(n, h->device), 256, 0, st>>>(C.p, n);
         PG_LAUNCH_CHECK();
         for (;;) {   // HOOK -> LINK -> ... until a HOOK pass hooks nothing
             PG_CK(cudaMemsetAsync(cnt.p, 0, 8, st));
@@ -210,7 +214,7 @@ void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uin
                 k_cc_hook<<<g, 256, 0, st>>>(d_bl.p, (int)bl.size(), rows, h->d_col.p, h->d_rowptr.p, C.p, cnt.p);
                 PG_LAUNCH_CHECK();
             }
-            k_cc_link<<<grid1(n), 256, 0, st>>>(C.p, n);
+            k_cc_link<<<grid1(n, h->device), 256, 0, st>>>(C.p, n);
             PG_LAUNCH_CHECK();
             unsigned long long hooks = 0;
             PG_CK(cudaMemcpyAsync(&hooks, cnt.p, 8, cudaMemcpyDeviceToHost, st));
@@ -220,12 +224,13 @@ void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uin
         }
         PG_CK(cudaMemsetAsync(M.p, 0xff, (size_t)n * 4, st));
         PG_CK(cudaMemsetAsync(cnt.p + 1, 0, 8, st));
-        k_cc_minorig<<<grid1(n), 256, 0, st>>>(h->d_rank.p, C.p, n, M.p);
+        k_cc_minorig<<<grid1(n, h->device), 256, 0, st>>>(h->d_rank.p, C.p, n, M.p);
         PG_LAUNCH_CHECK();
-        k_cc_labels<<<grid1(n), 256, 0, st>>>(h->d_rank.p, C.p, M.p, n, out, cnt.p + 1);
+        k_cc_labels<<<grid1(n, h->device), 256, 0, st>>>(h->d_rank.p, C.p, M.p, n, out, cnt.p + 1);
         PG_LAUNCH_CHECK();
     }
     PG_CK(cudaEventRecord(h->ev3, st));
+    end_call(h, st);
     unsigned long long nc = 0;
     if (n) PG_CK(cudaMemcpyAsync(&nc, cnt.p + 1, 8, cudaMemcpyDeviceToHost, st));
     if (!on_dev && n) PG_CK(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, st));

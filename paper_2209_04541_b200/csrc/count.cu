@@ -1017,6 +1017,38 @@ __global__ void k_clustering(const uint32_t* __restrict__ deg, const unsigned lo
 
 }  // namespace
 
+int sm_count(int device) {
+    static thread_local int dev = -1, sms = 0;
+    if (dev != device) {
+        PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        dev = device;
+    }
+    return sms;
+}
+
+void begin_call(pgabb_blocks_s* h, cudaStream_t st) {
+    if (h->ev_last_recorded) PG_CK(cudaStreamWaitEvent(st, h->ev_last, 0));
+}
+
+void end_call(pgabb_blocks_s* h, cudaStream_t st) {
+    PG_CK(cudaEventRecord(h->ev_last, st));
+    h->ev_last_recorded = true;
+}
+
+// Before a call re-records ev0..ev3: a previous async call's timing is read if its
+// events have completed, else dropped (never waited for -- a new call must not
+// stall the host on the previous one).
+void settle_timing(pgabb_blocks_s* h) {
+    if (!h->timing_pending) return;
+    const cudaError_t q = cudaEventQuery(h->ev3);
+    if (q == cudaSuccess) {
+        resolve_timing(h);
+        return;
+    }
+    if (q != cudaErrorNotReady) PG_CK(q);
+    h->timing_pending = false;
+}
+
 void resolve_timing(pgabb_blocks_s* h) {
     if (!h->timing_pending) return;
     PG_CK(cudaEventSynchronize(h->ev3));
@@ -1108,14 +1140,20 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
     };
 
+    settle_timing(h);
+    begin_call(h, st);
     PG_CK(cudaEventRecord(h->ev0, st));
     if (!h->streaming) {
         // S9: host-resident blocks are copied in for this call.
+        // Only the blocks this rank's pieces read (h->host_copies, merged ranges).
         if (h->residency == PGABB_RESIDENT_HOST && h->d_col.n) {
-            PG_CK(cudaMemcpyAsync(h->d_col.p, h->h_col.p, h->d_col.bytes(), cudaMemcpyHostToDevice, st));
-            PG_CK(cudaMemcpyAsync(h->d_rowptr.p, h->h_rowptr.p, h->d_rowptr.bytes(), cudaMemcpyHostToDevice, st));
-            PG_CK(cudaMemcpyAsync(h->d_bitmap.p, h->h_bitmap.p, h->d_bitmap.bytes(), cudaMemcpyHostToDevice, st));
-            h->h2d_last = h->d_col.bytes() + h->d_rowptr.bytes() + h->d_bitmap.bytes();
+            uint32_t* dpool[3] = {h->d_col.p, h->d_rowptr.p, h->d_bitmap.p};
+            const uint32_t* hpool[3] = {h->h_col.p, h->h_rowptr.p, h->h_bitmap.p};
+            for (const StagedBlock& c : h->host_copies) {
+                PG_CK(cudaMemcpyAsync(dpool[c.pool] + c.dst_word, hpool[c.pool] + c.src_word, c.words * 4,
+                                      cudaMemcpyHostToDevice, st));
+                h->h2d_last += c.words * 4;
+            }
         }
         PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
         if (vtx) PG_CK(cudaMemsetAsync(tv, 0, (size_t)h->n * sizeof(unsigned long long), st));
@@ -1184,7 +1222,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             h->launches_last++;
             {
                 const unsigned lg = (unsigned)std::max<unsigned long long>(
-                    1ull, std::min<unsigned long long>(148ull * 8, (wv.rows + kLightThreads - 1) / kLightThreads));
+                    1ull, std::min<unsigned long long>((unsigned long long)sm_count(h->device) * 8, (wv.rows + kLightThreads - 1) / kLightThreads));
                 light_kernel(true)<<<lg, kLightThreads, 0, st>>>(
                     nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
                     h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv,
@@ -1200,13 +1238,14 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     PG_LAUNCH_CHECK();
     h->launches_last++;
     if (vtx && h->n) {
-        k_gather_tv<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, 148 * 16), 256, 0, st>>>(
+        k_gather_tv<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, (uint64_t)sm_count(h->device) * 16), 256, 0, st>>>(
             h->d_rank.p, tv, h->n, d_tv_out, (opts && (opts->flags & PGABB_OUT_ACCUMULATE)) ? 1 : 0);
         PG_LAUNCH_CHECK();
         h->launches_last++;
     }
     PG_CK(cudaMemcpyAsync(h->h_result.p, h->d_task_counts.p + nt, 8, cudaMemcpyDeviceToHost, st));
     PG_CK(cudaEventRecord(h->ev3, st));
+    end_call(h, st);
     h->timing_pending = true;
     if (async) {
         *wrote = false;
@@ -1215,7 +1254,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     resolve_timing(h);
     if (opts && opts->task_counts && nt) {
         std::vector<unsigned long long> tc(nt);
-        PG_CK(cudaMemcpy(tc.data(), h->d_task_counts.p, nt * 8, cudaMemcpyDeviceToHost));
+        PG_COPY_SYNC(tc.data(), h->d_task_counts.p, nt * 8, st);
         for (int t = 0; t < nt; ++t) opts->task_counts[t] = tc[t];
     }
     *wrote = true;
@@ -1231,7 +1270,7 @@ void task_times(pgabb_blocks_s* h, uint64_t* ns) {
     bool wrote = false;
     count_triangles(h, nullptr, &wrote, nullptr, cyc.p);
     std::vector<unsigned long long> c(2 * nt);
-    PG_CK(cudaMemcpy(c.data(), cyc.p, 2 * nt * 8, cudaMemcpyDeviceToHost));
+    PG_COPY_SYNC(c.data(), cyc.p, 2 * nt * 8, h->stream);
     long double sh = 0, sl = 0;
     for (size_t t = 0; t < nt; ++t) {
         sh += c[t];
@@ -1262,9 +1301,11 @@ void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const u
         tvp = d_tv.p;
         ccp = d_cc.p;
     }
-    k_clustering<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, 148 * 16), 256, 0, st>>>(h->d_deg.p, tvp,
-                                                                                         h->n, ccp);
+    begin_call(h, st);
+    k_clustering<<<(unsigned)std::min<uint64_t>((h->n + 255) / 256, (uint64_t)sm_count(h->device) * 16), 256, 0, st>>>(
+        h->d_deg.p, tvp, h->n, ccp);
     PG_LAUNCH_CHECK();
+    end_call(h, st);
     if (!on_dev) PG_CK(cudaMemcpyAsync(cc, d_cc.p, (size_t)h->n * 8, cudaMemcpyDeviceToHost, st));
     PG_CK(cudaStreamSynchronize(st));
 }

@@ -24,6 +24,15 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 #define PG_CK(x) ::pgabb::check_cuda((x), #x, __FILE__, __LINE__)
 #define PG_LAUNCH_CHECK() ::pgabb::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
+// Blocking copy ORDERED ON `st` (cudaMemcpyDefault, UVA).  The handle's stream is
+// non-blocking, so a plain (legacy-stream) cudaMemcpy would not wait for the work
+// queued on it: every host read of a buffer the library filled goes through here.
+#define PG_COPY_SYNC(dst, src, bytes, st)                                                      \
+    do {                                                                                       \
+        PG_CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDefault, (st)));                \
+        PG_CK(cudaStreamSynchronize(st));                                                      \
+    } while (0)
+
 constexpr int kMaxParts = 64;          // p <= 64 (tid table p^3 entries)
 constexpr uint32_t kNoTask = 0xffffffffu;
 
@@ -229,6 +238,10 @@ struct pgabb_blocks_s {
     pgabb::DBuf<uint32_t> d_rowptr;             // rowptr pool (block-local edge offsets)
     pgabb::DBuf<uint32_t> d_bitmap;             // dense-block bitmap pool (rows of bm_words)
     pgabb::HBuf<uint32_t> h_col, h_rowptr, h_bitmap;   // host-resident copies (RESIDENT_HOST)
+    // RESIDENT_HOST without a budget: the pool ranges of the blocks this rank's pieces
+    // read (merged), copied host->device by every count (S9) -- a rank never copies
+    // blocks only other ranks' pieces need
+    std::vector<pgabb::StagedBlock> host_copies;
 
     // this rank's work list
     std::vector<pgabb::PieceDev> work;
@@ -254,6 +267,11 @@ struct pgabb_blocks_s {
     pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev_mid = nullptr;
+    // end of the last call's work on the handle's scratch (task counts, counters,
+    // arenas, t(v)); every call first waits for it on its own stream, so calls on
+    // different streams never overlap on the scratch (pgabb::begin_call / end_call)
+    cudaEvent_t ev_last = nullptr;
+    bool ev_last_recorded = false;
 
     // stats
     uint64_t cost_total = 0, cost_local = 0, alg_total = 0, alg_local = 0;
@@ -281,4 +299,8 @@ void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uin
                           uint32_t* iters);
 void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc);
 void resolve_timing(pgabb_blocks_s* h);
+void settle_timing(pgabb_blocks_s* h);
+void begin_call(pgabb_blocks_s* h, cudaStream_t st);
+void end_call(pgabb_blocks_s* h, cudaStream_t st);
+int sm_count(int device);   // multiprocessors of `device` (cached)
 }  // namespace pgabb

@@ -70,10 +70,13 @@ def combine_vertex_counts_host(local, group=None):
 
 
 def build_blocks_balanced(n, src, dst, p=0, cut_rule=0, group=None, **kw):
-    """S8 with measured task estimates (DESIGN R22): rank 0 times every task on a
-    1-rank handle (pgabb_task_times), broadcasts the per-task nanoseconds, and
-    every rank plans its LPT share with them -- the same plan everywhere, balanced
-    by device time instead of the S7 merge cost.  Untimed pre-processing."""
+    """S8 with measured task estimates (DESIGN R22): rank 0 alone builds a 1-rank
+    handle and times every task on it (pgabb_task_times), broadcasts the per-task
+    nanoseconds, and every rank plans its LPT share with them -- the same plan
+    everywhere, balanced by device time instead of the S7 merge cost.  Untimed
+    pre-processing.  The returned handle carries the weights as
+    ``task_weights_used`` (another handle of the same plan, e.g. host-resident,
+    is built with them)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -82,21 +85,32 @@ def build_blocks_balanced(n, src, dst, p=0, cut_rule=0, group=None, **kw):
     dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
     if ws <= 1:
         return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, **kw)
-    with build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev) as b1:
-        ns = b1.task_times() if rank == 0 else np.zeros(b1.ntasks, np.uint64)
+    ns = None
+    if rank == 0:
+        with build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev) as b1:
+            ns = b1.task_times()
     w = broadcast_weights(ns, group)
-    return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,
-                        task_weights=w, **kw)
+    b = build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,
+                     task_weights=w, **kw)
+    b.task_weights_used = w
+    return b
 
 
 def broadcast_weights(ns, group=None):
-    """Rank 0's per-task estimates to every rank (int64 over the group's backend)."""
+    """Rank 0's per-task estimates to every rank (int64 over the group's backend).
+    Only rank 0 needs ``ns``: the length is broadcast first."""
     import numpy as np
     import torch
     import torch.distributed as dist
-    t = torch.from_numpy(np.ascontiguousarray(ns, dtype=np.uint64).astype(np.int64))
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
-        if dist.get_backend(group) == "nccl":
-            t = t.cuda()
-        dist.broadcast(t, src=0, group=group)
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return np.ascontiguousarray(ns, dtype=np.uint64)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    rank = dist.get_rank(group)
+    k = torch.tensor([len(ns) if rank == 0 else 0], dtype=torch.int64, device=dev)
+    dist.broadcast(k, src=0, group=group)
+    if rank == 0:
+        t = torch.from_numpy(np.ascontiguousarray(ns, dtype=np.uint64).astype(np.int64)).to(dev)
+    else:
+        t = torch.zeros(int(k.item()), dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=0, group=group)
     return t.cpu().numpy().astype(np.uint64)
