@@ -23,7 +23,12 @@ def to_bytes(s):
     return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[u]
 
 
-def main(tag, config, rnd="01"):
+def main(tag, config, rnd="01", src_hash=None):
+    """src_hash: bench.kernel_src_hash() of the sources the capture ran (default: now)."""
+    if src_hash is None:
+        sys.path.insert(0, ROOT)
+        from bench import kernel_src_hash
+        src_hash = kernel_src_hash()
     g = os.path.join(ROOT, "gpurun_out")
     out = {"tag": tag, "config": config}
     bj = os.path.join(g, f"bench_{tag}.json")
@@ -52,9 +57,16 @@ def main(tag, config, rnd="01"):
             out[f"ncu_{kname}"] = k
             traffic = to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"])
             out[f"dram_bytes_per_launch_{kname}"] = traffic
+            stalls = {q.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v.split()[0] or 0)
+                      for q, v in k.items() if q.startswith("smsp__pcsamp_warps_issue_stalled_")
+                      and not q.endswith("_not_issued")}
+            top = max(stalls, key=stalls.get) if stalls else None
             entry[kname] = {"dram_bytes_per_launch": traffic, "source": f"profiles/r{rnd}_{tag}.json",
                             "l2_hit_pct": k.get("lts__t_sector_hit_rate.pct"),
-                            "kernel_ms_under_ncu": k.get("gpu__time_duration.sum")}
+                            "kernel_ms_under_ncu": k.get("gpu__time_duration.sum"),
+                            "issue_active_pct": k.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                            "warp_inst_per_launch": float(k["smsp__inst_executed.sum"].split()[0]),
+                            "top_stall": top, "src_hash": src_hash}
         js[config] = entry
         json.dump(js, open(ns, "w"), indent=1, sort_keys=True)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)

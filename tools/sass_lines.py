@@ -1,7 +1,7 @@
 """Attribute an ncu SASS source page (instructions executed, stall samples) to CUDA
 source lines, using nvdisasm's line info for the kernel in the cubin.
 
-    python tools/sass_lines.py <ncu-rep> <cubin> <kernel-substring>
+    python tools/sass_lines.py <ncu-rep> <cubin> <kernel-substring (mangled, for the cubin)> [<ncu kernel regex>]
 """
 import csv
 import io
@@ -29,10 +29,10 @@ def line_map(cubin, kname):
     return mapping
 
 
-def main(rep, cubin, kname):
+def main(rep, cubin, kname, ncu_kname=None):
     mp = line_map(cubin, kname)
     raw = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                                   "-k", f"regex:{kname}"], text=True)
+                                   "-k", f"regex:{ncu_kname or kname}"], text=True)
     rows = list(csv.reader(io.StringIO(raw)))
     hi = next(k for k, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hi]
