@@ -186,21 +186,123 @@ def task_alg_bytes(B, t) -> int:
     return int(total)
 
 
+# Reading R25 -- the orientation of a task's intersections.  Listing 5
+# fixes WHAT a task sums, |A_ix[u] ∩ A_jx[v]| over (u,v) in
+# A_ij, not which list is held and which is streamed.  LOW (the listing's own
+# loop order): per row u of part i hold A_ix[u], stream A_jx[v] for every v in
+# A_ij[u].  MID: per row v of part j hold A_jx[v], and for every u with (u,v) in
+# A_ij stream only the part of A_ix[u] that can close a triangle, the ids w > v:
+# A_jx[v] holds only ids > v (the DAG runs low -> high, R4), so no other w can
+# be common.  When x > j every id of part x is > v; when x == j (A_ix = A_ij)
+# it is the suffix of A_ij[u] after v.  Both sum the same intersections.
+LOW, MID = 0, 1
+
+
+def column(B, i, j, v):
+    """(u, e): the rows u of part i with (u, v) in A_ij, ascending, and the
+    block-local position e of (u, v) in A_ij's col array."""
+    rp, col = B[(i, j)]
+    e = np.nonzero(col == v)[0]
+    u = np.searchsorted(rp, e, side="right") - 1
+    return u, e
+
+
+def streamed_mid(B, t, u, v, e) -> int:
+    """|{w in A_ix[u] : w > v}| (only the ids that can be in A_jx[v])."""
+    i, j, x = t
+    if x > j:
+        return int(row(B, i, x, u).size)
+    rp = B[(i, j)][0]
+    return int(rp[u + 1] - (e + 1))
+
+
+def task_streams(B, t):
+    """(S_low, S_mid): the ids each orientation streams, summed over (u,v) in A_ij:
+    S_low = sum |A_jx[v]|, S_mid = sum |{w in A_ix[u] : w > v}|."""
+    i, j, x = t
+    rp_jx = B[(j, x)][0]
+    s_low = s_mid = 0
+    rp_ij, col = B[(i, j)]
+    for u in range(rp_ij.size - 1):
+        for e in range(rp_ij[u], rp_ij[u + 1]):
+            v = col[e]
+            s_low += int(rp_jx[v + 1] - rp_jx[v])
+            s_mid += streamed_mid(B, t, u, v, e)
+    return s_low, s_mid
+
+
+def orientation(B, t, orient=0) -> int:
+    """orient 1 = LOW, 2 = MID, 0 = auto: MID iff it streams fewer ids (S_mid < S_low)."""
+    if orient == 1:
+        return LOW
+    if orient == 2:
+        return MID
+    s_low, s_mid = task_streams(B, t)
+    return MID if s_mid < s_low else LOW
+
+
+def row_costs_mid(B, t) -> np.ndarray:
+    """rowcost(v), local rows v of part j: |A_jx[v]| (held once) if some u has
+    (u,v) in A_ij, plus sum over those u of |{w in A_ix[u] : w > v}|."""
+    i, j, x = t
+    rp_jx = B[(j, x)][0]
+    nrows = rp_jx.size - 1
+    out = np.zeros(nrows, np.int64)
+    for v in range(nrows):
+        us, es = column(B, i, j, v)
+        if us.size == 0:
+            continue
+        out[v] = int(rp_jx[v + 1] - rp_jx[v]) + sum(streamed_mid(B, t, u, v, e) for u, e in zip(us, es))
+    return out
+
+
+def task_cost_mid(B, t) -> int:
+    return int(row_costs_mid(B, t).sum())
+
+
+def task_alg_bytes_mid(B, t) -> int:
+    """Staged model of a MID task (R25, the R19 model with the roles swapped): over
+    the rows v of part j with A_jx[v] and column v of A_ij both non-empty,
+    4*(|A_jx[v]| + sum over those u of |{w in A_ix[u] : w > v}|) + 12 per u."""
+    i, j, x = t
+    rp_jx = B[(j, x)][0]
+    total = 0
+    for v in range(rp_jx.size - 1):
+        lv = int(rp_jx[v + 1] - rp_jx[v])
+        us, es = column(B, i, j, v)
+        if lv == 0 or us.size == 0:
+            continue
+        total += 4 * (lv + sum(streamed_mid(B, t, u, v, e) for u, e in zip(us, es))) + 12 * us.size
+    return int(total)
+
+
+def out_out_wedges(n: int, D: np.ndarray) -> int:
+    """sum_u C(d+(u), 2): the pairs v < w of out-neighbours of a vertex (in rank
+    space), i.e. what MID streams over all tasks at p = 1."""
+    if D.size == 0:
+        return 0
+    dp = np.bincount(D[:, 0], minlength=n).astype(np.int64)
+    return int((dp * (dp - 1) // 2).sum())
+
+
 # S8 -- pieces and LPT (PAPER.md:756-757, 843-849 §4.1/§4.4 "sorts them in
 # decreasing order"; reading R18).
-def pieces(B, tasks_, costs, G: int, weights=None):
+def pieces(B, tasks_, costs, G: int, weights=None, dirs=None):
     """[(task_idx, row_begin, row_end, weight)] in (task, row) order; zero-cost dropped.
 
     weights (reading R22): the scheduler's task estimates E(t) (PAPER.md:843-846,
     "E functor if defined"); None means E(t) = the S7 cost.  cap = ceil(total E /
     (4G)); a task with E(t) > cap is cut into k = ceil(E(t)/cap) row ranges at
-    row-cost quantiles, and a range's weight is floor(E(t) * its row cost / cost)."""
+    row-cost quantiles, and a range's weight is floor(E(t) * its row cost / cost).
+    dirs[ti] (reading R25): the task's orientation -- its rows are those of part i
+    (LOW, row costs R17) or of part j (MID, row costs R25); None = all LOW."""
     E = [int(c) for c in costs] if weights is None else [int(w) for w in weights]
     total = sum(E[ti] for ti in range(len(tasks_)) if int(costs[ti]) > 0)
     cap = None if G <= 1 else max(1, -(-total // (4 * G)))
     out = []
     for ti, t in enumerate(tasks_):
-        nrows = B[(t[0], t[1])][0].size - 1
+        d = LOW if dirs is None else dirs[ti]
+        nrows = B[(t[0], t[1])][0].size - 1 if d == LOW else B[(t[1], t[1])][0].size - 1
         cost = int(costs[ti])
         if cost == 0:
             continue
@@ -209,7 +311,7 @@ def pieces(B, tasks_, costs, G: int, weights=None):
             out.append((ti, 0, nrows, w))
             continue
         k = -(-w // cap)
-        R = np.concatenate([[0], np.cumsum(row_costs(B, t))])
+        R = np.concatenate([[0], np.cumsum(row_costs(B, t) if d == LOW else row_costs_mid(B, t))])
         bnd = [0]
         for q in range(1, k):
             bnd.append(int(np.searchsorted(k * R, q * cost, side="left")))
@@ -234,11 +336,13 @@ def lpt(pieces_, G: int):
     return owner, loads
 
 
-def piece_count(B, t, r0: int, r1: int) -> int:
+def piece_count(B, t, r0: int, r1: int, orient: int = LOW) -> int:
+    """Count of the piece's rows: rows u of part i (LOW) or rows v of part j (MID)."""
     i, j, x = t
     c = 0
     u_all, v_all = _edges(B, i, j)
-    sel = (u_all >= r0) & (u_all < r1)
+    r_all = u_all if orient == LOW else v_all
+    sel = (r_all >= r0) & (r_all < r1)
     for u, v in zip(u_all[sel], v_all[sel]):
         c += np.intersect1d(row(B, i, x, u), row(B, j, x, v), assume_unique=True).size
     return int(c)
@@ -247,7 +351,7 @@ def piece_count(B, t, r0: int, r1: int) -> int:
 class Plan:
     """All intermediate objects of the block method for one (graph, p, rule, G)."""
 
-    def __init__(self, n, src, dst, p, rule=0, G=1, weights=None, reverse=False):
+    def __init__(self, n, src, dst, p, rule=0, G=1, weights=None, reverse=False, orient=1):
         self.n = int(n)
         self.E = canonical_edges(n, src, dst)
         self.deg = degrees(n, self.E)
@@ -257,10 +361,14 @@ class Plan:
         self.cuts = cuts(n, self.D, self.p, rule)
         self.B = blocks(self.D, self.cuts)
         self.tasks = tasks(self.B, self.p)
-        self.costs = [task_cost(self.B, t) for t in self.tasks]
-        self.alg_bytes = [task_alg_bytes(self.B, t) for t in self.tasks]
+        # reading R25: each task's orientation, then its cost and bytes in it
+        self.dirs = [orientation(self.B, t, orient) for t in self.tasks]
+        self.costs = [task_cost(self.B, t) if d == LOW else task_cost_mid(self.B, t)
+                      for t, d in zip(self.tasks, self.dirs)]
+        self.alg_bytes = [task_alg_bytes(self.B, t) if d == LOW else task_alg_bytes_mid(self.B, t)
+                          for t, d in zip(self.tasks, self.dirs)]
         self.G = G
-        self.pieces = pieces(self.B, self.tasks, self.costs, G, weights)
+        self.pieces = pieces(self.B, self.tasks, self.costs, G, weights, self.dirs)
         self.owner, self.loads = lpt(self.pieces, G)
 
     def task_counts(self):

@@ -281,3 +281,89 @@ def test_pieces_partition_tasks(G):
     for pc, o in zip(P.pieces, P.owner):
         per_rank[o] += ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2])
     assert sum(per_rank) == oracle.count(*g)
+
+
+# ---- R25 orientation: MID holds A_jx[v] and streams only ids w > v ------------------
+def _wedge_counts(P, t):
+    """Direct enumeration over the DAG (not the blocks): S_low = #{(u,v,w): (u,v) in
+    A_ij, (v,w) in the DAG with w in part x}; S_mid = #{(u,v,w): (u,v), (u,w) in the
+    DAG, v < w, u in part i, v in part j, w in part x}."""
+    i, j, x = t
+    out = {}
+    for a, b in P.D:
+        out.setdefault(int(a), []).append(int(b))
+    part = lambda r: int(ob.part_of(P.cuts, r))
+    s_low = s_mid = 0
+    for u, vs in out.items():
+        if part(u) != i:
+            continue
+        for v in vs:
+            if part(v) != j:
+                continue
+            s_low += sum(1 for w in out.get(v, []) if part(w) == x)
+            s_mid += sum(1 for w in vs if w > v and part(w) == x)
+    return s_low, s_mid
+
+
+@pytest.mark.parametrize("g", [gen.rmat(7, 8, 1), gen.er(150, 12, 2), gen.complete(9), gen.king(6, 7)])
+def test_mid_streams_p1_out_out_wedges(g):
+    # p = 1: MID streams every pair v < w of out-neighbours of u once: sum_u C(d+(u), 2);
+    # LOW streams d+(v) per DAG edge (u,v): W = sum_v d-(v) d+(v)
+    P = ob.Plan(*g, p=1)
+    if not P.tasks:
+        return
+    s_low, s_mid = ob.task_streams(P.B, P.tasks[0])
+    assert s_mid == ob.out_out_wedges(P.n, P.D)
+    assert s_low == ob.wedges_dag(P.n, P.D)
+
+
+@pytest.mark.parametrize("p", [2, 3, 5])
+def test_mid_streams_vs_wedge_enumeration(p):
+    g = gen.rmat(7, 8, 5)
+    P = ob.Plan(*g, p=p)
+    for t in P.tasks:
+        assert ob.task_streams(P.B, t) == _wedge_counts(P, t)
+
+
+def test_mid_costs_k4_by_hand():
+    # K4, p = 1: DAG 0->{1,2,3}, 1->{2,3}, 2->{3}.  Rows v of MID:
+    #   v=1: column {0}; |A[1]| = 2 + ids of A[0] after 1 = {2,3}: 2      -> 4
+    #   v=2: column {0,1}; |A[2]| = 1 + {3} + {3}                         -> 3
+    #   v=3: column {0,1,2}; |A[3]| = 0 + nothing after 3                 -> 0
+    # cost 7; bytes: v=1 4*(2+2)+12, v=2 4*(1+2)+24 (v=3 holds nothing) = 64.
+    # Streams: S_low = sum over edges of |A[v]| = 2+1+0+1+0+0 = 4, S_mid = C(3,2)+C(2,2) = 4:
+    # a tie, so auto keeps LOW.
+    P = ob.Plan(*gen.complete(4), p=1, orient=2)
+    t = P.tasks[0]
+    assert list(ob.row_costs_mid(P.B, t)) == [0, 4, 3, 0]
+    assert P.costs == [7] and P.alg_bytes == [64] and P.dirs == [ob.MID]
+    assert ob.task_streams(P.B, t) == (4, 4)
+    assert ob.Plan(*gen.complete(4), p=1, orient=0).dirs == [ob.LOW]
+
+
+def test_auto_orientation_picks_fewer_streams():
+    g = gen.rmat(9, 16, 3)
+    P = ob.Plan(*g, p=4, orient=0)
+    assert ob.MID in P.dirs
+    for t, d in zip(P.tasks, P.dirs):
+        s_low, s_mid = ob.task_streams(P.B, t)
+        assert d == (ob.MID if s_mid < s_low else ob.LOW)
+
+
+@pytest.mark.parametrize("orient", [0, 2])
+@pytest.mark.parametrize("G", [1, 3])
+def test_mid_pieces_partition_tasks(orient, G):
+    g = gen.rmat(9, 16, 7)
+    P = ob.Plan(*g, p=3, G=G, orient=orient)
+    tc = P.task_counts()
+    for ti, t in enumerate(P.tasks):
+        d = P.dirs[ti]
+        mine = [pc for pc in P.pieces if pc[0] == ti]
+        assert sum(pc[3] for pc in mine) == P.costs[ti]
+        assert sum(ob.piece_count(P.B, t, pc[1], pc[2], d) for pc in mine) == tc[ti]
+        nrows = int(P.cuts[t[0] + 1] - P.cuts[t[0]]) if d == ob.LOW else int(P.cuts[t[1] + 1] - P.cuts[t[1]])
+        assert mine[0][1] == 0 and mine[-1][2] == nrows
+        for a, b in zip(mine, mine[1:]):
+            assert a[2] <= b[1]
+    total = sum(ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2], P.dirs[pc[0]]) for pc in P.pieces)
+    assert total == oracle.count(*g)
