@@ -42,6 +42,8 @@ def parse(argv=None):
                     help="c5 (Graph500 R-MAT s26 ef32, the headline) | c2 | c3 | c4 | c1 | c5s")
     ap.add_argument("--p", type=int, default=0, help="override parts per dimension")
     ap.add_argument("--cut-rule", type=int, default=0)
+    ap.add_argument("--orient", default="auto", choices=["auto", "low", "mid"],
+                    help="task orientation (DESIGN R25): per task the one streaming fewer ids, or all LOW / MID")
     ap.add_argument("--path", choices=["count", "vertex", "vertex2", "cc"], default="count",
                     # vertex2: the two-pass route of R24 (measured far slower: kept for the record)
                     help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1); "
@@ -222,7 +224,8 @@ L2_NOTE = "L2 flushed (256 MiB write) between timed steps, outside the events"
 def workload_config(cfg, args, n, m_tuples, m_edges, p):
     """The workload keys, identical in both arms (ours and --impl reference)."""
     return {"workload": f"{cfg.name}: {cfg.desc}", "path": args.path, "n": n, "tuples": m_tuples,
-            "m_edges": m_edges, "p": p, "cut_rule": args.cut_rule, "l2": L2_NOTE}
+            "m_edges": m_edges, "p": p, "cut_rule": args.cut_rule, "orient": args.orient,
+            "l2": L2_NOTE}
 
 
 def run_reference(args):
@@ -393,12 +396,12 @@ def run_ours(args):
     if ws > 1 and args.balance == "measured":
         # S8 with rank 0's measured task times broadcast to all ranks (DESIGN R22; untimed)
         from paper_2209_04541_b200 import dist as pgd
-        b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule)
+        b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient)
     elif args.budget_gb > 0:
-        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
                             residency=pg.RESIDENT_HOST, device_budget_bytes=int(args.budget_gb * (1 << 30)))
     else:
-        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws)
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
     # a real (non-legacy-default) stream: the library orders its work on it and the
@@ -411,7 +414,7 @@ def run_ours(args):
     tv_dev = torch.zeros(max(n, 1), dtype=torch.int64, device="cuda") if vertex else None
     b_rev = None
     if args.path == "vertex2":   # the reversed-order handle of the two-pass route (R24)
-        b_rev = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+        b_rev = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
                                 reverse_order=True)
 
     def step():
@@ -494,7 +497,7 @@ def run_ours(args):
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
     if not args.no_e2e and not vertex and args.budget_gb <= 0:
-        bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=dev, rank=rank, world_size=ws,
+        bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
                              residency=pg.RESIDENT_HOST,
                              task_weights=getattr(b, "task_weights_used", None))
         for _ in range(max(1, args.warmup)):
@@ -583,7 +586,7 @@ def run_cc(args):
     cfg = CONFIGS[args.config]
     p = args.p or cfg.p
     n, s, d = cfg.generate()
-    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, device=0)
+    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=0)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
     lab = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")

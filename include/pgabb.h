@@ -103,7 +103,21 @@ typedef struct {
                                      Borrowed for the call. */
     uint64_t n_task_weights;      /* must equal the task count when task_weights != NULL
                                      (EINVAL otherwise) */
+    uint32_t orient;            /* task orientation (DESIGN R25; Listing 5, PAPER.md:689-697,
+                                   fixes what a task sums, not which list is held):
+                                   PGABB_ORIENT_AUTO (0, default) per task the one that
+                                   streams fewer ids; PGABB_ORIENT_LOW (1) hold A_ix[u] per
+                                   row u, stream A_jx[v] (no transposes are built);
+                                   PGABB_ORIENT_MID (2) hold A_jx[v] per row v, stream the
+                                   ids w > v of A_ix[u] for every (u,v) in A_ij (needs the
+                                   blocks' transposes: 2 more u32 per edge).  Counts are
+                                   identical for every value. */
+    uint32_t reserved0;
 } pgabb_build_opts_t;
+
+#define PGABB_ORIENT_AUTO 0u
+#define PGABB_ORIENT_LOW 1u
+#define PGABB_ORIENT_MID 2u
 
 /* Fills *opts with the defaults (p=0->8, rule 0, current device, one rank, HBM). */
 PGABB_API void pgabb_default_build_opts(pgabb_build_opts_t* opts);
@@ -260,8 +274,15 @@ PGABB_API pgabb_status_t pgabb_get_block(pgabb_blocks_t b, uint32_t i, uint32_t 
  * any output may be NULL. */
 PGABB_API pgabb_status_t pgabb_get_tasks(pgabb_blocks_t b, uint32_t* ijx, uint64_t* cost,
                                uint64_t* alg_bytes);
+/* Task orientations (DESIGN R25): dir[t] (0 LOW, 1 MID) and the ids each orientation
+ * streams, s_low[t] = sum over (u,v) in A_ij of |A_jx[v]|, s_mid[t] = sum of
+ * |{w in A_ix[u] : w > v}| (0 when the handle has no transposes, orient LOW); any
+ * output may be NULL. */
+PGABB_API pgabb_status_t pgabb_get_task_orient(pgabb_blocks_t b, uint32_t* dir, uint64_t* s_low,
+                                     uint64_t* s_mid);
 /* Pieces (S8) in (task, row) order: task[k], row_begin[k], row_end[k] (local rows of
- * part i), cost[k], owner[k] (rank); any output may be NULL. */
+ * part i for a LOW task, of part j for a MID task), cost[k], owner[k] (rank); any
+ * output may be NULL. */
 PGABB_API pgabb_status_t pgabb_get_pieces(pgabb_blocks_t b, uint32_t* task, uint32_t* row_begin,
                                 uint32_t* row_end, uint64_t* cost, int32_t* owner);
 

@@ -232,13 +232,15 @@ def task_streams(B, t):
 
 
 def orientation(B, t, orient=0) -> int:
-    """orient 1 = LOW, 2 = MID, 0 = auto: MID iff it streams fewer ids (S_mid < S_low)."""
+    """orient 1 = LOW, 2 = MID, 0 = auto: MID iff it streams at most 3/4 of LOW's
+    ids (4 S_mid < 3 S_low; a MID row reads its neighbours from the transpose, and
+    near-equal streams measured faster in LOW -- ER, DESIGN R25)."""
     if orient == 1:
         return LOW
     if orient == 2:
         return MID
     s_low, s_mid = task_streams(B, t)
-    return MID if s_mid < s_low else LOW
+    return MID if 4 * s_mid < 3 * s_low else LOW
 
 
 def row_costs_mid(B, t) -> np.ndarray:

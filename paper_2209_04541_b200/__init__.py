@@ -237,8 +237,20 @@ class Blocks:
         k = self.ntasks
         return ijx[:3 * k].reshape(k, 3), cost[:k], alg[:k]
 
+    def task_orient(self):
+        """(dir[ntasks] 0 LOW / 1 MID, s_low[ntasks], s_mid[ntasks]) -- DESIGN R25."""
+        nt = max(self.ntasks, 1)
+        d = np.empty(nt, np.uint32)
+        sl = np.empty(nt, np.uint64)
+        sm = np.empty(nt, np.uint64)
+        _ck(_lib.pgabb_get_task_orient(self._h, d.ctypes.data_as(_abi.u32p), sl.ctypes.data_as(_abi.u64p),
+                                       sm.ctypes.data_as(_abi.u64p)), "pgabb_get_task_orient")
+        k = self.ntasks
+        return d[:k], sl[:k], sm[:k]
+
     def pieces(self):
-        """list of (task, row_begin, row_end, cost) and owner list."""
+        """list of (task, row_begin, row_end, cost) and owner list (rows of part i for
+        a LOW task, of part j for a MID task)."""
         npc = int(self.stats()["npieces"])
         m = max(npc, 1)
         t, r0, r1 = (np.empty(m, np.uint32) for _ in range(3))
@@ -251,10 +263,17 @@ class Blocks:
         return pcs, [int(o[k]) for k in range(npc)]
 
 
+ORIENTS = {"auto": 0, "low": 1, "mid": 2}
+
+
 def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = -1, rank: int = 0,
                  world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0,
-                 task_weights=None, reverse_order: bool = False) -> Blocks:
+                 task_weights=None, reverse_order: bool = False, orient="auto") -> Blocks:
     """S1..S8: canonicalise, degree-order, orient, cut, block, enumerate, cost, assign.
+
+    orient: task orientation (DESIGN R25) -- "auto" (per task, fewer streamed ids),
+    "low" (hold A_ix[u], stream A_jx[v]; no transposes) or "mid" (hold A_jx[v],
+    stream the ids w > v of A_ix[u]); also 0 / 1 / 2.
 
     src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device).
     task_weights: optional per-task estimates E(t) (e.g. Blocks.task_times() of a
@@ -271,6 +290,7 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     o.inputs_on_device = int(sdev)
     o.rank, o.world_size, o.residency = rank, world_size, residency
     o.reverse_order = int(bool(reverse_order))
+    o.orient = ORIENTS[orient] if isinstance(orient, str) else int(orient)
     o.device_budget_bytes = device_budget_bytes
     tw = None
     if task_weights is not None:

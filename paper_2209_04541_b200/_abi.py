@@ -32,7 +32,8 @@ OUT_ACCUMULATE = 32
 class BuildOpts(ctypes.Structure):
     _fields_ = [("p", u32), ("cut_rule", u32), ("device", i32), ("inputs_on_device", u32),
                 ("rank", i32), ("world_size", i32), ("residency", u32), ("reverse_order", u32),
-                ("device_budget_bytes", u64), ("task_weights", u64p), ("n_task_weights", u64)]
+                ("device_budget_bytes", u64), ("task_weights", u64p), ("n_task_weights", u64),
+                ("orient", u32), ("reserved0", u32)]
 
 
 class CountOpts(ctypes.Structure):
@@ -69,6 +70,7 @@ SIGNATURES = [
     ("pgabb_get_cuts", ctypes.c_int, [vp, u32p]),
     ("pgabb_get_block", ctypes.c_int, [vp, u32, u32, u32p, u32p, u64p]),
     ("pgabb_get_tasks", ctypes.c_int, [vp, u32p, u64p, u64p]),
+    ("pgabb_get_task_orient", ctypes.c_int, [vp, u32p, u64p, u64p]),
     ("pgabb_get_pieces", ctypes.c_int, [vp, u32p, u32p, u32p, u64p, i32p]),
     ("pgabb_free", None, [vp]),
     ("pgabb_last_error", ctypes.c_char_p, []),
@@ -82,6 +84,8 @@ def load():
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, res, args in SIGNATURES:
+        if os.environ.get("PGABB_LIB_VARIANT") and not hasattr(lib, name):
+            continue   # A/B runs against an older build of the library (tools/variants.py)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -60,7 +60,6 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_rank.release();
     d_col.release();
     d_rowptr.release();
-    d_work.release();
     d_task_counts.release();
     d_next.release();
     h_col.release();
@@ -142,6 +141,8 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->residency = o.residency;
         if (o.reverse_order > 1) fail(PGABB_EINVAL, "reverse_order must be 0 or 1");
         h->reverse_order = o.reverse_order;
+        if (o.orient > PGABB_ORIENT_MID) fail(PGABB_EINVAL, "orient must be 0 (auto), 1 (low) or 2 (mid)");
+        h->orient = o.orient;
         h->budget = o.device_budget_bytes;
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
         if (o.task_weights) h->task_weights.assign(o.task_weights, o.task_weights + o.n_task_weights);
@@ -336,6 +337,18 @@ pgabb_status_t pgabb_get_tasks(pgabb_blocks_t b, uint32_t* ijx, uint64_t* cost, 
             if (ijx) { ijx[3 * t] = T.i; ijx[3 * t + 1] = T.j; ijx[3 * t + 2] = T.x; }
             if (cost) cost[t] = T.cost;
             if (alg) alg[t] = T.alg_bytes;
+        }
+    });
+}
+
+pgabb_status_t pgabb_get_task_orient(pgabb_blocks_t b, uint32_t* dir, uint64_t* s_low, uint64_t* s_mid) {
+    return guarded([&] {
+        if (!b) fail(PGABB_EINVAL, "NULL argument");
+        for (size_t t = 0; t < b->tasks.size(); ++t) {
+            const Task& T = b->tasks[t];
+            if (dir) dir[t] = T.dir;
+            if (s_low) s_low[t] = T.s_low;
+            if (s_mid) s_mid[t] = T.s_mid;
         }
     });
 }

@@ -267,6 +267,140 @@ __global__ void k_task_costs(CostArg a, int i, int j) {
     }
 }
 
+// ---- S5c transposes (DESIGN R25, MID orientation) ---------------------------
+// key = block id << 32 | local col v, value = the edge's position k in the
+// block-major col pool; a stable sort by key orders each block's entries by
+// (v, u) (u ascending within a column, as the pool is (u, v)-sorted per block).
+__global__ void k_tkeys(const uint64_t* dag, uint64_t mE, int B, CutsArg cu, const uint32_t* col, uint64_t* key,
+                        uint32_t* val) {
+    const uint64_t mask = (1ull << B) - 1;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = dag[k];
+        const uint32_t b = (uint32_t)(part_of(cu, (uint32_t)(d >> B)) * cu.p + part_of(cu, (uint32_t)(d & mask)));
+        key[k] = ((uint64_t)b << 32) | col[k];
+        val[k] = (uint32_t)k;
+    }
+}
+
+// tcol[pos] = u (local row of part i), tpos[pos] = k - col_off (block-local position
+// of (u,v) in col).  The sorted entries of block b occupy the block's own range.
+__global__ void k_tfill(const uint64_t* dag, uint64_t mE, int B, CutsArg cu, const uint64_t* key,
+                        const uint32_t* val, const unsigned long long* off, uint32_t* tcol, uint32_t* tpos) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < mE;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = val[q];
+        const uint32_t b = (uint32_t)(key[q] >> 32);
+        const uint32_t i = b / (uint32_t)cu.p;
+        tcol[q] = (uint32_t)(dag[k] >> B) - cu.c[i];
+        tpos[q] = (uint32_t)(k - off[b]);
+    }
+}
+
+// transposed rowptr of the present blocks: entry t of block b (ncols + 1 entries)
+// = number of b's entries with local col < t (lower bound over the sorted keys).
+struct TBlockDev {
+    unsigned long long off, nnz, trp_off;
+    uint32_t ncols, bid;
+};
+__global__ void k_trowptr(const uint64_t* key, const TBlockDev* blk, const unsigned long long* start, int nblk,
+                          unsigned long long total, uint32_t* rowptr) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nblk;   // last block with start <= t
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (start[mid] <= t) lo = mid; else hi = mid;
+        }
+        const TBlockDev bd = blk[lo];
+        const uint64_t target = ((uint64_t)bd.bid << 32) | (uint64_t)(t - start[lo]);
+        uint64_t a = 0, z = bd.nnz;
+        const uint64_t* kk = key + bd.off;
+        while (a < z) {
+            const uint64_t mid = a + ((z - a) >> 1);
+            if (kk[mid] < target) a = mid + 1; else z = mid;
+        }
+        rowptr[bd.trp_off + (t - start[lo])] = (uint32_t)a;
+    }
+}
+
+// S7 for the MID orientation (R25), one thread per entry of the transpose of a
+// non-empty block (i, j) (warp-uniform x-loop as k_task_costs): entry (v, u, e);
+// s = |{w in A_ix[u] : w > v}| (= |A_ix[u]| when x > j, the suffix after e when
+// x == j); the column's first entry also adds the held |A_jx[v]|.
+struct CostMidArg {
+    const uint32_t* col;          // col pool (the tcol / tpos regions at tcol_base / tpos_base)
+    const uint32_t* rowptr;
+    const BlockDev* blk;          // indexed by block id i*p+j
+    const uint32_t* tid;          // p^3
+    int p;
+    unsigned long long tcol_base, tpos_base;
+    unsigned long long *cost, *alg_bytes, *s_low, *s_mid;
+};
+__global__ void k_task_costs_mid(CostMidArg a, int i, int j) {
+    const BlockDev bij = a.blk[i * a.p + j];
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = warp0; base < bij.nnz; base += stride) {
+        const uint64_t q = bij.col_off + base + lane;
+        const bool ok = base + lane < bij.nnz;
+        uint32_t u = 0, v = 0, e = 0;
+        bool first = false;
+        if (ok) {
+            u = a.col[a.tcol_base + q];
+            e = a.col[a.tpos_base + q];
+            v = a.col[bij.col_off + e];
+            first = (q == bij.col_off) || (a.col[bij.col_off + a.col[a.tpos_base + q - 1]] != v);
+        }
+        for (int x = j; x < a.p; ++x) {
+            const uint32_t t = a.tid[(i * a.p + j) * a.p + x];
+            if (t == kNoTask) continue;
+            unsigned long long c = 0, by = 0, sl = 0, sm = 0;
+            if (ok) {
+                const BlockDev bix = a.blk[i * a.p + x], bjx = a.blk[j * a.p + x];
+                const uint32_t lb = a.rowptr[bjx.rp_off + v + 1] - a.rowptr[bjx.rp_off + v];
+                const uint32_t s = (x == j) ? a.rowptr[bij.rp_off + u + 1] - (e + 1)
+                                            : a.rowptr[bix.rp_off + u + 1] - a.rowptr[bix.rp_off + u];
+                c = s + (first ? lb : 0u);
+                if (lb) by = 4ull * (s + (first ? lb : 0u)) + 12ull;
+                sl = lb;
+                sm = s;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                c += __shfl_down_sync(0xffffffffu, c, o);
+                by += __shfl_down_sync(0xffffffffu, by, o);
+                sl += __shfl_down_sync(0xffffffffu, sl, o);
+                sm += __shfl_down_sync(0xffffffffu, sm, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.cost[t], c);
+                atomicAdd(&a.alg_bytes[t], by);
+                atomicAdd(&a.s_low[t], sl);
+                atomicAdd(&a.s_mid[t], sm);
+            }
+        }
+    }
+}
+
+// S8 helper for a MID task: rowcost(v) over the rows v of part j (R25).
+__global__ void k_row_costs_mid(const uint32_t* col, const uint32_t* rowptr, uint64_t tcol_base, uint64_t tpos_base,
+                                BlockDev bij, uint64_t trp_ij, uint32_t ncols, BlockDev bix, BlockDev bjx, int same,
+                                unsigned long long* rc) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < ncols;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q0 = rowptr[trp_ij + v], q1 = rowptr[trp_ij + v + 1];
+        unsigned long long s = 0;
+        if (q1 > q0) s = rowptr[bjx.rp_off + v + 1] - rowptr[bjx.rp_off + v];
+        for (uint32_t q = q0; q < q1; ++q) {
+            const uint32_t u = col[tcol_base + bij.col_off + q];
+            const uint32_t e = col[tpos_base + bij.col_off + q];
+            s += same ? rowptr[bij.rp_off + u + 1] - (e + 1) : rowptr[bix.rp_off + u + 1] - rowptr[bix.rp_off + u];
+        }
+        rc[v + 1] = s;
+    }
+}
+
 // S8 helper: row costs of one task (for splitting heavy tasks into pieces).
 __global__ void k_row_costs(const uint32_t* col, const uint32_t* rowptr, BlockDev bij, BlockDev bix,
                             BlockDev bjx, unsigned long long* rc) {
@@ -299,41 +433,50 @@ __global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsig
     }
 }
 
-// Row items of one owned piece: rows u in [r0, r1) with A_ij[u] and A_ix[u]
-// non-empty, classified by their work (DESIGN R20): LIGHT rows -- |A_ix[u]| <=
-// kLightLa, |A_ij[u]| <= kLightLe and at most kLightWork list loads for the
-// thread-per-row kernel (a v list of <= kLightScan ids is scanned, a longer one
-// is binary-searched per element of A_ix[u]; a dense A_jx costs one bit test per
-// element) -- get lf = 1; every other row gets hf = 1 (warp per row).
+// Row items of one owned piece, in kernel roles (TaskDev, R25): rows r in [r0, r1)
+// with a non-empty held list S and neighbour list, classified by their work
+// (DESIGN R20): LIGHT rows -- |S| <= kLightLa, <= kLightLe neighbours and at most
+// kLightWork list loads for the thread-per-row kernel (a streamed list of <=
+// kLightScan ids is scanned, a longer one binary-searched per element of S; a
+// dense streamed block costs one bit test per element) -- get lf = 1; every other
+// row gets hf = its number of heavy items (neighbour chunks, warp per item).
 // hf[nrows] = lf[nrows] = 0 for the exclusive scans.
-// alg (nullable): += staged-model bytes of the light rows (DESIGN R19), for the
-// per-kernel roofline.
-__global__ void k_row_flags(PieceDev w, const uint32_t* col, const uint32_t* rowptr, int dense_jx, uint32_t* hf,
-                            uint32_t* lf, unsigned long long* alg) {
+// alg (nullable): += staged-model bytes of the light rows (DESIGN R19/R25), for
+// the per-kernel roofline.
+__device__ __forceinline__ uint32_t streamed_len(const TaskDev& T, const uint32_t* col, const uint32_t* rowptr,
+                                                 uint32_t e) {
+    const uint32_t nb = col[T.n_col + e];
+    const uint32_t end = rowptr[T.t_rp + nb + 1];
+    const uint32_t beg = T.n_pos != ~0ull ? col[T.n_pos + e] + 1 : rowptr[T.t_rp + nb];
+    return end - beg;
+}
+
+__global__ void k_row_flags(PieceDev w, const TaskDev* tasks, const uint32_t* col, const uint32_t* rowptr,
+                            uint32_t* hf, uint32_t* lf, unsigned long long* alg) {
+    const TaskDev T = tasks[w.task];
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k0 = blockIdx.x * (uint64_t)blockDim.x; k0 <= nr; k0 += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = k0 + threadIdx.x;
         uint32_t fh = 0, fl = 0;
         unsigned long long bytes = 0;
         if (k < nr) {
-            const uint32_t u = w.r0 + (uint32_t)k;
-            const uint32_t e0 = rowptr[w.rp_ij + u], e1 = rowptr[w.rp_ij + u + 1];
-            const uint32_t la = rowptr[w.rp_ix + u + 1] - rowptr[w.rp_ix + u];
+            const uint32_t r = w.r0 + (uint32_t)k;
+            const uint32_t e0 = rowptr[T.n_rp + r], e1 = rowptr[T.n_rp + r + 1];
+            const uint32_t la = rowptr[T.s_rp + r + 1] - rowptr[T.s_rp + r];
             if (e1 > e0 && la > 0) {
                 bool light = la <= kLightLa && e1 - e0 <= kLightLe;
                 if (light) {
                     uint32_t work = 0, lsum = 0;
                     for (uint32_t e = e0; e < e1; ++e) {
-                        const uint32_t v = col[w.col_ij + e];
-                        const uint32_t lb = rowptr[w.rp_jx + v + 1] - rowptr[w.rp_jx + v];
+                        const uint32_t lb = streamed_len(T, col, rowptr, e);
                         work += light_pair_loads(la, lb);
                         lsum += lb;
                     }
-                    light = dense_jx || work <= kLightWork;
+                    light = T.t_bm != ~0ull || work <= kLightWork;
                     bytes = 4ull * (la + lsum) + 12ull * (e1 - e0);
                 }
                 fl = light;
-                fh = !light;
+                fh = light ? 0u : heavy_chunks(e1 - e0);
                 if (!light) bytes = 0;
             }
         }
@@ -348,24 +491,26 @@ __global__ void k_row_flags(PieceDev w, const uint32_t* col, const uint32_t* row
     }
 }
 
-__global__ void k_row_emit(PieceDev w, const uint32_t* flags, const uint32_t* pos, unsigned long long* out) {
+__global__ void k_row_emit(PieceDev w, const uint32_t* nchunks, const uint32_t* pos, unsigned long long* out) {
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nr;
          k += (uint64_t)gridDim.x * blockDim.x)
-        if (flags[k]) out[pos[k]] = ((unsigned long long)w.task << 32) | (w.r0 + (uint32_t)k);
+        for (uint32_t c = 0; c < nchunks[k]; ++c)
+            out[pos[k] + c] = ((unsigned long long)w.task << 48) | ((unsigned long long)c << 32) | (w.r0 + (uint32_t)k);
 }
 
 // Light items of one owned piece (16 bytes each, see internal.h).
-__global__ void k_light_emit(PieceDev w, const uint32_t* flags, const uint32_t* pos, const uint32_t* rowptr,
-                             uint4* out) {
+__global__ void k_light_emit(PieceDev w, const TaskDev* tasks, const uint32_t* flags, const uint32_t* pos,
+                             const uint32_t* rowptr, uint4* out) {
+    const TaskDev T = tasks[w.task];
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nr;
          k += (uint64_t)gridDim.x * blockDim.x)
         if (flags[k]) {
-            const uint32_t u = w.r0 + (uint32_t)k;
-            const uint32_t a0 = rowptr[w.rp_ix + u], la = rowptr[w.rp_ix + u + 1] - a0;
-            const uint32_t e0 = rowptr[w.rp_ij + u], le = rowptr[w.rp_ij + u + 1] - e0;
-            out[pos[k]] = make_uint4(w.task | (la << kLightTaskBits) | (le << (kLightTaskBits + 4)), a0, e0, u);
+            const uint32_t r = w.r0 + (uint32_t)k;
+            const uint32_t a0 = rowptr[T.s_rp + r], la = rowptr[T.s_rp + r + 1] - a0;
+            const uint32_t e0 = rowptr[T.n_rp + r], le = rowptr[T.n_rp + r + 1] - e0;
+            out[pos[k]] = make_uint4(w.task | (la << kLightTaskBits) | (le << (kLightTaskBits + 4)), a0, e0, r);
         }
 }
 
@@ -569,8 +714,14 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         k_block_offsets<<<grid_for(nb + 1), kThreads, 0, st>>>(bid2.p, mE, nb, d_off.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaMemcpyAsync(off.data(), d_off.p, (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
-        h->d_col.alloc(mE + kColPad);   // padded: the kernels read 16-byte covers of lists
-        PG_CK(cudaMemsetAsync(h->d_col.p + mE, 0, kColPad * 4, st));
+        // padded: the kernels read 16-byte covers of lists.  With the transposes (R25)
+        // the pool holds three regions of mE + kColPad words: cols, tcol, tpos.
+        h->has_t = h->orient != 1;
+        const uint64_t region = mE + kColPad;
+        h->tcol_base = h->has_t ? region : 0;
+        h->tpos_base = h->has_t ? 2 * region : 0;
+        h->d_col.alloc(h->has_t ? 3 * region : region);
+        PG_CK(cudaMemsetAsync(h->d_col.p, 0, h->d_col.bytes(), st));
         k_local_cols<<<grid_for(mE), kThreads, 0, st>>>(dag2.p, bid2.p, mE, B, cu, h->d_col.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaStreamSynchronize(st));
@@ -590,6 +741,7 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
             b.col_off = off[i * p + j];
             b.nnz = off[i * p + j + 1] - off[i * p + j];
             b.nrows = h->cuts[i + 1] - h->cuts[i];
+            b.ncols = h->cuts[j + 1] - h->cuts[j];
             b.present = (b.nnz > 0);
             if (b.present) {
                 b.rp_off = rp_total;
@@ -599,8 +751,21 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
             bdev[i * p + j] = to_dev(b, h->cuts[i]);
             if (b.present) present.push_back(bdev[i * p + j]);
         }
+    const uint64_t rp_plain = rp_total;
+    std::vector<TBlockDev> tpresent;
+    std::vector<unsigned long long> trp_start;
+    if (h->has_t)
+        for (uint32_t i = 0; i < p; ++i)
+            for (uint32_t j = i; j < p; ++j) {
+                BlockInfo& b = h->blocks[i * p + j];
+                if (!b.present) continue;
+                b.trp_off = rp_total;
+                trp_start.push_back(rp_total - rp_plain);
+                tpresent.push_back(TBlockDev{b.col_off, b.nnz, b.trp_off, b.ncols, i * p + j});
+                rp_total += (uint64_t)b.ncols + 1;
+            }
     h->d_rowptr.alloc(std::max<uint64_t>(rp_total, 1));
-    if (rp_total) {
+    if (rp_plain) {
         DBuf<BlockDev> d_present;
         DBuf<unsigned long long> d_rps;
         d_present.alloc(present.size());
@@ -608,8 +773,45 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_CK(cudaMemcpyAsync(d_present.p, present.data(), present.size() * sizeof(BlockDev),
                               cudaMemcpyHostToDevice, st));
         PG_CK(cudaMemcpyAsync(d_rps.p, rp_start.data(), rp_start.size() * 8, cudaMemcpyHostToDevice, st));
-        k_rowptr<<<grid_for(rp_total), kThreads, 0, st>>>(dag, B, d_present.p, d_rps.p, (int)present.size(),
-                                                          rp_total, h->d_rowptr.p);
+        k_rowptr<<<grid_for(rp_plain), kThreads, 0, st>>>(dag, B, d_present.p, d_rps.p, (int)present.size(),
+                                                          rp_plain, h->d_rowptr.p);
+        PG_LAUNCH_CHECK();
+        PG_CK(cudaStreamSynchronize(st));
+    }
+
+    // ---- S5c transposes of the blocks (MID orientation, DESIGN R25) ----------
+    if (h->has_t && mE) {
+        DBuf<uint64_t> tk, tk2;
+        DBuf<uint32_t> tv, tv2;
+        tk.alloc(mE);
+        tv.alloc(mE);
+        k_tkeys<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, h->d_col.p, tk.p, tv.p);
+        PG_LAUNCH_CHECK();
+        tk2.alloc(mE);
+        tv2.alloc(mE);
+        const int bbits = std::max(1, bits_for(nb - 1));
+        cub_call([&](void* t, size_t& b) {   // stable: u order kept within a column
+            return cub::DeviceRadixSort::SortPairs(t, b, tk.p, tk2.p, tv.p, tv2.p, (int64_t)mE, 0, 32 + bbits, st);
+        }, st, tmp);
+        tk.release();
+        tv.release();
+        DBuf<unsigned long long> d_off;
+        d_off.alloc(nb + 1);
+        PG_CK(cudaMemcpyAsync(d_off.p, off.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
+        k_tfill<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, tk2.p, tv2.p, d_off.p, h->d_col.p + h->tcol_base,
+                                                    h->d_col.p + h->tpos_base);
+        PG_LAUNCH_CHECK();
+        const uint64_t ttotal = rp_total - rp_plain;
+        DBuf<TBlockDev> d_tb;
+        DBuf<unsigned long long> d_ts;
+        d_tb.alloc(tpresent.size());
+        d_ts.alloc(trp_start.size());
+        PG_CK(cudaMemcpyAsync(d_tb.p, tpresent.data(), tpresent.size() * sizeof(TBlockDev), cudaMemcpyHostToDevice,
+                              st));
+        PG_CK(cudaMemcpyAsync(d_ts.p, trp_start.data(), trp_start.size() * 8, cudaMemcpyHostToDevice, st));
+        // entry t of the flattened transposed rowptrs -> block by start, then lower bound
+        k_trowptr<<<grid_for(ttotal), kThreads, 0, st>>>(tk2.p, d_tb.p, d_ts.p, (int)tpresent.size(), ttotal,
+                                                         h->d_rowptr.p);
         PG_LAUNCH_CHECK();
         PG_CK(cudaStreamSynchronize(st));
     }
@@ -678,16 +880,50 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
                 k_task_costs<<<grid_for(b.nnz), kThreads, 0, st>>>(a, (int)i, (int)j);
                 PG_LAUNCH_CHECK();
             }
-        std::vector<unsigned long long> c(nt), ae(nt);
+        std::vector<unsigned long long> c(nt), ae(nt), cm(nt, 0), am(nt, 0), sl(nt, 0), sm(nt, 0);
         PG_CK(cudaMemcpyAsync(c.data(), d_cost.p, nt * 8, cudaMemcpyDeviceToHost, st));
         PG_CK(cudaMemcpyAsync(ae.data(), d_alg.p, nt * 8, cudaMemcpyDeviceToHost, st));
         PG_CK(cudaStreamSynchronize(st));
+        if (h->has_t) {   // R25: the MID orientation's cost, bytes and streamed ids
+            DBuf<unsigned long long> d_cm, d_am, d_sl, d_sm;
+            for (auto* d : {&d_cm, &d_am, &d_sl, &d_sm}) {
+                d->alloc(nt);
+                PG_CK(cudaMemsetAsync(d->p, 0, nt * 8, st));
+            }
+            CostMidArg am_{};
+            am_.col = h->d_col.p; am_.rowptr = h->d_rowptr.p; am_.blk = d_blk.p; am_.tid = d_tid.p; am_.p = (int)p;
+            am_.tcol_base = h->tcol_base; am_.tpos_base = h->tpos_base;
+            am_.cost = d_cm.p; am_.alg_bytes = d_am.p; am_.s_low = d_sl.p; am_.s_mid = d_sm.p;
+            for (uint32_t i = 0; i < p; ++i)
+                for (uint32_t j = i; j < p; ++j) {
+                    const BlockInfo& b = h->blocks[i * p + j];
+                    if (!b.present) continue;
+                    k_task_costs_mid<<<grid_for(b.nnz), kThreads, 0, st>>>(am_, (int)i, (int)j);
+                    PG_LAUNCH_CHECK();
+                }
+            PG_CK(cudaMemcpyAsync(cm.data(), d_cm.p, nt * 8, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaMemcpyAsync(am.data(), d_am.p, nt * 8, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaMemcpyAsync(sl.data(), d_sl.p, nt * 8, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaMemcpyAsync(sm.data(), d_sm.p, nt * 8, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaStreamSynchronize(st));
+        }
         h->cost_total = 0;
         h->alg_total = 0;
         for (size_t t = 0; t < nt; ++t) {
             Task& T = h->tasks[t];
-            T.cost = c[t];
-            T.alg_bytes = ae[t];
+            T.cost_low = c[t];
+            T.alg_low = ae[t];
+            T.cost_mid = cm[t];
+            T.alg_mid = am[t];
+            T.s_low = sl[t];
+            T.s_mid = sm[t];
+            // R25: orient 1 -> LOW, 2 -> MID, 0 (auto) -> MID iff it streams at most 3/4
+            // of LOW's ids (near-equal streams measured faster in LOW: ER c3)
+            T.dir = !h->has_t ? kDirLow
+                    : h->orient == 2 ? kDirMid
+                                     : ((unsigned __int128)4 * sm[t] < (unsigned __int128)3 * sl[t] ? kDirMid : kDirLow);
+            T.cost = T.dir == kDirMid ? T.cost_mid : T.cost_low;
+            T.alg_bytes = T.dir == kDirMid ? T.alg_mid : T.alg_low;
             h->cost_total += T.cost;
             h->alg_total += T.alg_bytes;
         }
@@ -720,18 +956,23 @@ void plan_pieces(pgabb_blocks_s* h) {
         const BlockInfo& bij = h->blocks[T.i * p + T.j];
         if (T.cost == 0) continue;   // no (u,v,x) with a non-empty list: count 0
         const uint64_t w = E(t);
+        const uint32_t nr = T.dir == kDirMid ? bij.ncols : bij.nrows;   // rows of part i (LOW) / j (MID)
         if (w <= cap) {
-            h->pieces.push_back(Piece{(uint32_t)t, 0, bij.nrows, w, 0, T.cost});
+            h->pieces.push_back(Piece{(uint32_t)t, 0, nr, w, 0, T.cost});
             continue;
         }
         const uint64_t k = (w + cap - 1) / cap;
-        const uint32_t nr = bij.nrows;
         rc.alloc((size_t)nr + 1);
         R.alloc((size_t)nr + 1);
         PG_CK(cudaMemsetAsync(rc.p, 0, ((size_t)nr + 1) * 8, st));
-        k_row_costs<<<grid_for(nr), kThreads, 0, st>>>(h->d_col.p, h->d_rowptr.p, to_dev(bij, h->cuts[T.i]),
-                                                       to_dev(h->blocks[T.i * p + T.x], 0),
-                                                       to_dev(h->blocks[T.j * p + T.x], 0), rc.p);
+        if (T.dir == kDirMid)
+            k_row_costs_mid<<<grid_for(nr), kThreads, 0, st>>>(
+                h->d_col.p, h->d_rowptr.p, h->tcol_base, h->tpos_base, to_dev(bij, h->cuts[T.i]), bij.trp_off, nr,
+                to_dev(h->blocks[T.i * p + T.x], 0), to_dev(h->blocks[T.j * p + T.x], 0), (int)(T.x == T.j), rc.p);
+        else
+            k_row_costs<<<grid_for(nr), kThreads, 0, st>>>(h->d_col.p, h->d_rowptr.p, to_dev(bij, h->cuts[T.i]),
+                                                           to_dev(h->blocks[T.i * p + T.x], 0),
+                                                           to_dev(h->blocks[T.j * p + T.x], 0), rc.p);
         PG_LAUNCH_CHECK();
         cub_call([&](void* tp, size_t& b) {
             return cub::DeviceScan::InclusiveSum(tp, b, rc.p, R.p, (int64_t)nr + 1, st);
@@ -779,6 +1020,87 @@ void plan_pieces(pgabb_blocks_s* h) {
     }
 }
 
+// ---- the blocks and parts a task reads in its orientation (S9) ---------------
+int task_parts(const pgabb_blocks_s* h, const Task& T, PartRef out[8]) {
+    const uint32_t p = h->p, bij = T.i * p + T.j, bix = T.i * p + T.x, bjx = T.j * p + T.x;
+    int n = 0;
+    auto add = [&](uint32_t b, int part) {
+        for (int k = 0; k < n; ++k)
+            if (out[k].block == b && out[k].part == part) return;
+        out[n++] = PartRef{b, part};
+    };
+    if (T.dir == kDirMid) {
+        add(bij, kPartTCol);
+        add(bij, kPartTRp);
+        if (T.x == T.j) add(bij, kPartTPos);
+        add(bjx, kPartCol);
+        add(bjx, kPartRp);
+        add(bix, kPartCol);
+        add(bix, kPartRp);
+        if (h->blocks[bix].bm_off != ~0ull) add(bix, kPartBm);
+    } else {
+        add(bij, kPartCol);
+        add(bij, kPartRp);
+        add(bix, kPartCol);
+        add(bix, kPartRp);
+        add(bjx, kPartCol);
+        add(bjx, kPartRp);
+        if (h->blocks[bjx].bm_off != ~0ull) add(bjx, kPartBm);
+    }
+    return n;
+}
+
+uint64_t part_words(const pgabb_blocks_s* h, PartRef r) {
+    const BlockInfo& B = h->blocks[r.block];
+    switch (r.part) {
+        case kPartCol: case kPartTCol: case kPartTPos: return B.nnz;
+        case kPartRp: return B.present ? (uint64_t)B.nrows + 1 : 0;
+        case kPartTRp: return B.present ? (uint64_t)B.ncols + 1 : 0;
+        default: return B.bm_off == ~0ull ? 0 : (uint64_t)B.nrows * B.bm_words;
+    }
+}
+
+uint64_t part_src(const pgabb_blocks_s* h, PartRef r, int* pool) {
+    const BlockInfo& B = h->blocks[r.block];
+    switch (r.part) {
+        case kPartCol: *pool = 0; return B.col_off;
+        case kPartTCol: *pool = 0; return h->tcol_base + B.col_off;
+        case kPartTPos: *pool = 0; return h->tpos_base + B.col_off;
+        case kPartRp: *pool = 1; return B.rp_off;
+        case kPartTRp: *pool = 1; return B.trp_off;
+        default: *pool = 2; return B.bm_off;
+    }
+}
+
+// A task's descriptor in kernel roles (internal.h TaskDev); off(part) = where the
+// part lives (its pool offset, or a wave's arena offset).
+template <class Off>
+static TaskDev make_taskdev(const pgabb_blocks_s* h, const Task& T, Off off) {
+    const uint32_t p = h->p, bij = T.i * p + T.j, bix = T.i * p + T.x, bjx = T.j * p + T.x;
+    TaskDev d{};
+    d.dir = T.dir;
+    d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
+    d.cx = h->cuts[T.x];
+    if (T.dir == kDirMid) {
+        d.s_col = off(PartRef{bjx, kPartCol}); d.s_rp = off(PartRef{bjx, kPartRp});
+        d.n_col = off(PartRef{bij, kPartTCol}); d.n_rp = off(PartRef{bij, kPartTRp});
+        d.n_pos = T.x == T.j ? off(PartRef{bij, kPartTPos}) : ~0ull;
+        d.t_col = off(PartRef{bix, kPartCol}); d.t_rp = off(PartRef{bix, kPartRp});
+        d.t_bm = h->blocks[bix].bm_off == ~0ull ? ~0ull : off(PartRef{bix, kPartBm});
+        d.bm_words = h->blocks[bix].bm_words;
+        d.c_row = h->cuts[T.j]; d.c_nbr = h->cuts[T.i];
+    } else {
+        d.s_col = off(PartRef{bix, kPartCol}); d.s_rp = off(PartRef{bix, kPartRp});
+        d.n_col = off(PartRef{bij, kPartCol}); d.n_rp = off(PartRef{bij, kPartRp});
+        d.n_pos = ~0ull;
+        d.t_col = off(PartRef{bjx, kPartCol}); d.t_rp = off(PartRef{bjx, kPartRp});
+        d.t_bm = h->blocks[bjx].bm_off == ~0ull ? ~0ull : off(PartRef{bjx, kPartBm});
+        d.bm_words = h->blocks[bjx].bm_words;
+        d.c_row = h->cuts[T.i]; d.c_nbr = h->cuts[T.j];
+    }
+    return d;
+}
+
 // Owned pieces in execution order: task (x desc, j desc, i asc), then rows.
 static std::vector<size_t> locality_order(const pgabb_blocks_s* h) {
     std::vector<size_t> order(h->work.size());
@@ -798,22 +1120,15 @@ static std::vector<size_t> locality_order(const pgabb_blocks_s* h) {
 // and its own task-descriptor table.  EBUDGET if one task's three blocks alone
 // exceed half the budget ("hard error").
 void plan_waves(pgabb_blocks_s* h) {
-    const uint32_t p = h->p;
     const uint64_t half = h->budget / 2 / 4;   // words per arena
     const size_t nt = h->tasks.size();
     h->waves.clear();
     std::vector<WavePiece> wpieces;
     std::vector<TaskDev> wtasks;
     const std::vector<size_t> order = locality_order(h);
-    auto block_words = [&](uint32_t b, int pool) -> uint64_t {
-        const BlockInfo& B = h->blocks[b];
-        if (pool == 0) return B.nnz;
-        if (pool == 1) return (uint64_t)B.nrows + 1;
-        return B.bm_off == ~0ull ? 0 : (uint64_t)B.nrows * B.bm_words;
-    };
-    struct Need { uint32_t b; int pool; };
-    std::map<std::pair<uint32_t, int>, uint64_t> placed;   // (block, pool) -> arena word offset
-    // the previous wave's placement: a block it holds is copied device-to-device
+    // (block, part) -> arena word offset of the current wave
+    std::map<std::pair<uint32_t, int>, uint64_t> placed;
+    // the previous wave's placement: a block part it holds is copied device-to-device
     // from the other arena instead of host-to-device (consecutive waves share blocks
     // by the locality order: NEXT-2 block reuse)
     std::map<std::pair<uint32_t, int>, uint64_t> prev_placed;
@@ -837,15 +1152,13 @@ void plan_waves(pgabb_blocks_s* h) {
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const Task& T = h->tasks[w.task];
-        const uint32_t bij = T.i * p + T.j, bix = T.i * p + T.x, bjx = T.j * p + T.x;
-        std::vector<Need> need = {{bij, 0}, {bij, 1}, {bix, 0}, {bix, 1}, {bjx, 0}, {bjx, 1}, {bjx, 2}};
+        PartRef parts[8];
+        const int np = task_parts(h, T, parts);
         uint64_t all = 0, fresh = 0;
-        std::set<std::pair<uint32_t, int>> uniq;
-        for (const Need& q : need) {
-            if (!uniq.insert({q.b, q.pool}).second) continue;
-            const uint64_t wd = block_words(q.b, q.pool);
+        for (int q = 0; q < np; ++q) {
+            const uint64_t wd = part_words(h, parts[q]);
             all += wd;
-            if (!placed.count({q.b, q.pool})) fresh += wd;
+            if (!placed.count({parts[q].block, parts[q].part})) fresh += wd;
         }
         if (all > half)
             fail(PGABB_EBUDGET, "task (" + std::to_string(T.i) + "," + std::to_string(T.j) + "," +
@@ -855,26 +1168,19 @@ void plan_waves(pgabb_blocks_s* h) {
             close_wave();
             open_wave();
         }
-        for (const auto& key : uniq) {
+        for (int q = 0; q < np; ++q) {
+            const std::pair<uint32_t, int> key{parts[q].block, parts[q].part};
             if (placed.count(key)) continue;
-            const uint64_t wd = block_words(key.first, key.second);
-            const BlockInfo& B = h->blocks[key.first];
-            const uint64_t src = key.second == 0 ? B.col_off : key.second == 1 ? B.rp_off : B.bm_off;
+            const uint64_t wd = part_words(h, parts[q]);
+            int pool = 0;
+            const uint64_t src = part_src(h, parts[q], &pool);
             placed[key] = cur.words;
             const auto pv = prev_placed.find(key);
             if (wd && pv != prev_placed.end()) cur.copies.push_back(StagedBlock{pv->second, cur.words, wd, 3});
-            else if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, key.second});
+            else if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, pool});
             cur.words += wd;
         }
-        TaskDev d{};
-        d.col_ij = placed[{bij, 0}]; d.rp_ij = placed[{bij, 1}];
-        d.col_ix = placed[{bix, 0}]; d.rp_ix = placed[{bix, 1}];
-        d.col_jx = placed[{bjx, 0}]; d.rp_jx = placed[{bjx, 1}];
-        d.bm_jx = h->blocks[bjx].bm_off == ~0ull ? ~0ull : placed[{bjx, 2}];
-        d.bm_words = h->blocks[bjx].bm_words;
-        d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
-        d.ci = h->cuts[T.i]; d.cj = h->cuts[T.j]; d.cx = h->cuts[T.x];
-        cur_tasks[w.task] = d;
+        cur_tasks[w.task] = make_taskdev(h, T, [&](PartRef r) { return placed[{r.block, r.part}]; });
         wpieces.push_back(WavePiece{cur.rows, w.task, w.r0});
         cur.rows += w.r1 - w.r0;
     }
@@ -893,31 +1199,39 @@ void plan_waves(pgabb_blocks_s* h) {
     }
 }
 
-// This rank's work list: owned pieces in (task, row) order with their pool offsets.
+// This rank's work list: owned pieces in (task, row) order, the task descriptors
+// (kernel roles, R25), the host-resident copy list (S9) and the row items.
 void upload_work(pgabb_blocks_s* h) {
-    const uint32_t p = h->p;
     const int me = std::max(0, h->rank);
+    cudaStream_t st = h->stream;
     h->work.clear();
     h->work_edges = 0;
     h->cost_local = 0;
     h->alg_local = 0;
+
+    // task descriptors for the intersection kernels (pool offsets)
+    std::vector<TaskDev> td(std::max<size_t>(h->tasks.size(), 1));
+    for (size_t t = 0; t < h->tasks.size(); ++t)
+        td[t] = make_taskdev(h, h->tasks[t], [&](PartRef r) {
+            int pool = 0;
+            return part_src(h, r, &pool);
+        });
+    h->d_tasks.alloc(td.size());
+    PG_COPY_SYNC(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), st);
+
     std::vector<char> task_mine(h->tasks.size(), 0);
     for (const Piece& pc : h->pieces) {
         if (pc.owner != me) continue;
-        const Task& T = h->tasks[pc.task];
-        const BlockInfo &bij = h->blocks[T.i * p + T.j], &bix = h->blocks[T.i * p + T.x],
-                        &bjx = h->blocks[T.j * p + T.x];
+        const TaskDev& T = td[pc.task];
         uint32_t e0 = 0, e1 = 0;
-        PG_COPY_SYNC(&e0, h->d_rowptr.p + bij.rp_off + pc.r0, 4, h->stream);
-        PG_COPY_SYNC(&e1, h->d_rowptr.p + bij.rp_off + pc.r1, 4, h->stream);
+        PG_COPY_SYNC(&e0, h->d_rowptr.p + T.n_rp + pc.r0, 4, st);
+        PG_COPY_SYNC(&e1, h->d_rowptr.p + T.n_rp + pc.r1, 4, st);
         if (e1 == e0) continue;
         PieceDev w{};
         w.gstart = h->work_edges;
-        w.col_ij = bij.col_off; w.rp_ij = bij.rp_off;
-        w.col_ix = bix.col_off; w.rp_ix = bix.rp_off;
-        w.col_jx = bjx.col_off; w.rp_jx = bjx.rp_off;
         w.r0 = pc.r0; w.r1 = pc.r1; w.e0 = e0; w.e1 = e1;
         w.task = pc.task;
+        w.dir = h->tasks[pc.task].dir;
         h->work.push_back(w);
         h->work_edges += (e1 - e0);
         h->cost_local += pc.cost;
@@ -933,28 +1247,25 @@ void upload_work(pgabb_blocks_s* h) {
             if (pc.task == t && pc.owner == me) mine += pc.rcost;
         h->alg_local += (uint64_t)((long double)T.alg_bytes * mine / (T.cost ? T.cost : 1));
     }
-    h->d_work.alloc(std::max<size_t>(h->work.size(), 1));
-    if (!h->work.empty())
-        PG_COPY_SYNC(h->d_work.p, h->work.data(), h->work.size() * sizeof(PieceDev), h->stream);
     h->d_task_counts.alloc(h->tasks.size() + 1);
     h->d_next.alloc(8);
 
-    // S9 (host-resident, no budget): the pool ranges of the blocks the owned pieces read
+    // S9 (host-resident, no budget): the pool ranges of the block parts the owned
+    // pieces read, merged
     {
-        std::vector<char> need((size_t)p * p, 0);
+        std::set<std::pair<uint32_t, int>> need;
         for (const PieceDev& w : h->work) {
-            const Task& T = h->tasks[w.task];
-            need[T.i * p + T.j] = need[T.i * p + T.x] = 1;
-            need[T.j * p + T.x] |= 2;   // bit 1: the v-side block (its dense copy is read too)
+            PartRef parts[8];
+            const int np = task_parts(h, h->tasks[w.task], parts);
+            for (int q = 0; q < np; ++q) need.insert({parts[q].block, parts[q].part});
         }
         std::vector<StagedBlock> r;
-        for (uint32_t b = 0; b < p * p; ++b) {
-            if (!need[b]) continue;
-            const BlockInfo& B = h->blocks[b];
-            if (B.nnz) r.push_back(StagedBlock{B.col_off, B.col_off, B.nnz, 0});
-            if (B.present) r.push_back(StagedBlock{B.rp_off, B.rp_off, (uint64_t)B.nrows + 1, 1});
-            if ((need[b] & 2) && B.bm_off != ~0ull)
-                r.push_back(StagedBlock{B.bm_off, B.bm_off, (uint64_t)B.nrows * B.bm_words, 2});
+        for (const auto& key : need) {
+            const PartRef pr{key.first, key.second};
+            const uint64_t wd = part_words(h, pr);
+            int pool = 0;
+            const uint64_t src = part_src(h, pr, &pool);
+            if (wd) r.push_back(StagedBlock{src, src, wd, pool});
         }
         std::sort(r.begin(), r.end(), [](const StagedBlock& a, const StagedBlock& b) {
             return a.pool != b.pool ? a.pool < b.pool : a.src_word < b.src_word;
@@ -971,49 +1282,22 @@ void upload_work(pgabb_blocks_s* h) {
         // padding the build wrote, and their ids are masked by the list bounds)
     }
 
-    // task descriptors for the intersection kernel
-    std::vector<TaskDev> td(std::max<size_t>(h->tasks.size(), 1));
-    for (size_t t = 0; t < h->tasks.size(); ++t) {
-        const Task& T = h->tasks[t];
-        const BlockInfo &bij = h->blocks[T.i * p + T.j], &bix = h->blocks[T.i * p + T.x],
-                        &bjx = h->blocks[T.j * p + T.x];
-        TaskDev d{};
-        d.col_ij = bij.col_off; d.rp_ij = bij.rp_off;
-        d.col_ix = bix.col_off; d.rp_ix = bix.rp_off;
-        d.col_jx = bjx.col_off; d.rp_jx = bjx.rp_off;
-        d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
-        d.bm_jx = bjx.bm_off;
-        d.bm_words = bjx.bm_words;
-        d.ci = h->cuts[T.i]; d.cj = h->cuts[T.j]; d.cx = h->cuts[T.x];
-        td[t] = d;
-    }
-    h->d_tasks.alloc(td.size());
-    PG_COPY_SYNC(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), h->stream);
-
     // largest block-triple footprint (what one task needs resident, S9)
     h->max_task_bytes = 0;
     for (const Task& T : h->tasks) {
-        const uint32_t ids[3] = {T.i * p + T.j, T.i * p + T.x, T.j * p + T.x};
-        uint64_t bytes = 0;
-        for (int a = 0; a < 3; ++a) {
-            bool dup = false;
-            for (int z = 0; z < a; ++z) dup |= (ids[z] == ids[a]);
-            if (dup) continue;
-            const BlockInfo& B = h->blocks[ids[a]];
-            bytes += 4 * (B.nnz + (uint64_t)B.nrows + 1);
-        }
-        const BlockInfo& J = h->blocks[ids[2]];
-        if (J.bm_off != ~0ull) bytes += 4ull * J.nrows * J.bm_words;
-        h->max_task_bytes = std::max(h->max_task_bytes, bytes);
+        PartRef parts[8];
+        const int np = task_parts(h, T, parts);
+        uint64_t words = 0;
+        for (int q = 0; q < np; ++q) words += part_words(h, parts[q]);
+        h->max_task_bytes = std::max(h->max_task_bytes, 4 * words);
     }
     if (h->streaming) return;   // streaming residency enumerates rows implicitly per wave
 
     // Row items of the owned pieces, laid out for L2 locality: pieces in task
     // order (x desc, j desc, i asc) so that the warps running concurrently share
-    // the v-side block A_jx (and the hub column part is done first), rows
-    // ascending inside a piece.  Compaction is a flag + exclusive scan per piece,
+    // the blocks of one task (and the hub column part is done first), rows
+    // ascending inside a piece.  Compaction is a count + exclusive scan per piece,
     // so the layout is deterministic.
-    cudaStream_t st = h->stream;
     const std::vector<size_t> order = locality_order(h);
     uint32_t maxrows = 0;
     for (const PieceDev& w : h->work) maxrows = std::max(maxrows, w.r1 - w.r0);
@@ -1029,9 +1313,8 @@ void upload_work(pgabb_blocks_s* h) {
     PG_CK(cudaMemsetAsync(d_alg.p, 0, 8, st));
     auto classify = [&](const PieceDev& w, unsigned long long* alg) {
         const uint32_t nr = w.r1 - w.r0;
-        const Task& T = h->tasks[w.task];
-        const int dense = h->blocks[T.j * h->p + T.x].bm_off != ~0ull;
-        k_row_flags<<<grid_for(nr + 1), kThreads, 0, st>>>(w, h->d_col.p, h->d_rowptr.p, dense, hf.p, lf.p, alg);
+        k_row_flags<<<grid_for(nr + 1), kThreads, 0, st>>>(w, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, hf.p, lf.p,
+                                                           alg);
         PG_LAUNCH_CHECK();
         cub_call([&](void* tp, size_t& b) {
             return cub::DeviceScan::ExclusiveSum(tp, b, hf.p, hpos.p, (int64_t)nr + 1, st);
@@ -1076,7 +1359,8 @@ void upload_work(pgabb_blocks_s* h) {
             PG_LAUNCH_CHECK();
         }
         if (piece_light[k]) {
-            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, lf.p, lpos.p, h->d_rowptr.p, h->d_light.p + lbase);
+            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_tasks.p, lf.p, lpos.p, h->d_rowptr.p,
+                                                            h->d_light.p + lbase);
             PG_LAUNCH_CHECK();
         }
         base += piece_items[k];

@@ -266,8 +266,12 @@ __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 3
 // VM (per-vertex roles, NEXT-1): VM >= 2 adds each pair's count c_uv to tvj[v],
 // VM >= 3 counts each common element w for w (warp counters, VCnt); the row
 // total goes to u in the caller (VM >= 1).  VM = 0 is exactly the counting kernel.
-template <int MODE, int R, int VM>
+// POS (MID tasks with x == j, R25): each neighbour's streamed list starts after the
+// row vertex, at npos[e] + 1, instead of at its rowptr (a compile-time switch: the
+// runtime select measured 7 % on every LOW launch)
+template <int MODE, int R, int VM, bool POS>
 __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ vcol, uint32_t e0, uint32_t e1,
+                                                  const uint32_t* __restrict__ npos,
                                                   const uint32_t* __restrict__ rp_jx,
                                                   const uint32_t* __restrict__ Bc,
                                                   const uint32_t* __restrict__ BM, uint32_t W, const uint32_t* S,
@@ -293,8 +297,10 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
         uint32_t v = 0, b0 = 0, lb = 0;
         if (e + lane < e1) {
             v = __ldg(vcol + e + lane);
-            b0 = __ldg(rp_jx + v);
-            lb = __ldg(rp_jx + v + 1) - b0;
+            const uint32_t bend = __ldg(rp_jx + v + 1);
+            // MID with x == j: the neighbour's list starts after the row vertex (R25)
+            b0 = POS ? __ldg(npos + e + lane) + 1 : __ldg(rp_jx + v);
+            lb = bend - b0;
         }
         PROF_MARK(9);
         // dense pairs: AND of bitmap rows
@@ -346,7 +352,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                         }
                     }
                     acc += cv;
-                    if (VM >= 2 && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
+                    if (VM >= 1 && tvj && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
                 }
             }
             if (use_and) lb = 0;
@@ -377,7 +383,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 }
             }
             acc += cv;
-            if (VM >= 2 && cv) atomicAdd(tvj + v, (unsigned long long)cv);
+            if (VM >= 1 && tvj && cv) atomicAdd(tvj + v, (unsigned long long)cv);
             if (use_search) lb = 0;
             PROF_MARK(4);
         }
@@ -406,7 +412,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             scratch[sidx] = (lo >> 2) - excl;
             scratch[32 + sidx] = lo;
             scratch[64 + sidx] = hi;
-            if (VM >= 2) scratch[96 + sidx] = v;
+            if (VM >= 1) scratch[96 + sidx] = v;
         }
         __syncwarp();
         for (uint32_t base = 0; base < total; base += 64) {
@@ -430,7 +436,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                     vpos[r] = pos + scratch[seg];
                     wlo[r] = scratch[32 + seg];
                     whi[r] = scratch[64 + seg];
-                    if (VM >= 2) vv[r] = scratch[96 + seg];
+                    if (VM >= 1) vv[r] = scratch[96 + seg];
                     x[r] = __ldg(V + vpos[r]);
                 }
             }
@@ -439,7 +445,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                 const int w0 = 4 * (int)vpos[r];
                 const uint32_t c = probe4<MODE, (VM >= 3)>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, vc);
                 acc += c;
-                if (VM >= 2 && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
+                if (VM >= 1 && tvj && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
             }
         }
         PROF_MARK(6);
@@ -478,7 +484,7 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
                 const uint32_t same = __match_any_sync(0xffffffffu, hit ? a : 0xffffffffu);
                 if (hit && lane == __ffs(same) - 1) atomicAdd(tvx + a, (unsigned long long)__popc(same));
             }
-            if (VM >= 2 && hit) atomicAdd(tvj + v, 1ull);
+            if (VM >= 1 && tvj && hit) atomicAdd(tvj + v, 1ull);
             q += dq;
             k += dk;
             if (k >= la) {
@@ -514,7 +520,7 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
             }
         }
         acc += cv;
-        if (VM >= 2 && cv) atomicAdd(tvj + v, (unsigned long long)cv);
+        if (VM >= 1 && tvj && cv) atomicAdd(tvj + v, (unsigned long long)cv);
     }
     return acc;
 }
@@ -546,16 +552,17 @@ __device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next
             t_l = wp[lo].task;
             u_l = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
             const TaskDev& T = tasks[t_l];
-            const uint32_t la = __ldg(rowptr + T.rp_ix + u_l + 1) - __ldg(rowptr + T.rp_ix + u_l);
-            const uint32_t e0 = __ldg(rowptr + T.rp_ij + u_l), e1 = __ldg(rowptr + T.rp_ij + u_l + 1);
+            const uint32_t la = __ldg(rowptr + T.s_rp + u_l + 1) - __ldg(rowptr + T.s_rp + u_l);
+            const uint32_t e0 = __ldg(rowptr + T.n_rp + u_l), e1 = __ldg(rowptr + T.n_rp + u_l + 1);
             heavy = la > 0 && e1 > e0;
             if (heavy && la <= kLightLa && e1 - e0 <= kLightLe) {
-                bool light = T.bm_jx != ~0ull;
+                bool light = T.t_bm != ~0ull;
                 if (!light) {
                     uint32_t work = 0;
                     for (uint32_t e = e0; e < e1; ++e) {
-                        const uint32_t v = __ldg(col + T.col_ij + e);
-                        work += light_pair_loads(la, __ldg(rowptr + T.rp_jx + v + 1) - __ldg(rowptr + T.rp_jx + v));
+                        const uint32_t v = __ldg(col + T.n_col + e);
+                        const uint32_t b0 = T.n_pos != ~0ull ? __ldg(col + T.n_pos + e) + 1 : __ldg(rowptr + T.t_rp + v);
+                        work += light_pair_loads(la, __ldg(rowptr + T.t_rp + v + 1) - b0);
                     }
                     light = work <= kLightWork;
                 }
@@ -576,6 +583,8 @@ __device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next
 // (VM >= 1), v each pair's c_uv (VM >= 2), w one per hit (VM >= 3) -- so with
 // VM = 3 the sum over ranks of tv is t(v) and sum tv = 3T.
 // TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
+#define IROW(M, R_, ...) \
+    (npos ? intersect_row<M, R_, VM, true>(__VA_ARGS__) : intersect_row<M, R_, VM, false>(__VA_ARGS__))
 template <bool IMPLICIT, int VM, bool TIMED>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
@@ -608,7 +617,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     unsigned long long pt = clock64();
 #endif
     for (;;) {
-        uint32_t t, u;
+        uint32_t t, u, chunk = 0;
         if (IMPLICIT) {
             if (!hrows && !(hrows = implicit_heavy_rows(next, nitems, wp, nwp, tasks, col, rowptr, lane, t_l, u_l)))
                 break;
@@ -619,29 +628,41 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         } else {
             if (idx >= nitems) break;
             const unsigned long long it = __ldg(items + idx);
-            t = (uint32_t)(it >> 32);
+            t = (uint32_t)(it >> 48);
+            chunk = (uint32_t)(it >> 32) & 0xffffu;
             u = (uint32_t)it;
             idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
         }
         const long long c0 = TIMED ? clock64() : 0;
+        // kernel roles (internal.h TaskDev, DESIGN R25): u is the item's row vertex,
+        // A its held list, vcol its neighbours (chunk `chunk` of them), Bc/rp_jx the
+        // neighbours' streamed lists, npos their suffix starts (MID, x == j)
         const TaskDev T = tasks[t];
-        const uint32_t a0 = __ldg(rowptr + T.rp_ix + u), a1 = __ldg(rowptr + T.rp_ix + u + 1);
-        const uint32_t e0 = __ldg(rowptr + T.rp_ij + u), e1 = __ldg(rowptr + T.rp_ij + u + 1);
+        const uint32_t a0 = __ldg(rowptr + T.s_rp + u), a1 = __ldg(rowptr + T.s_rp + u + 1);
+        uint32_t e0 = __ldg(rowptr + T.n_rp + u), e1 = __ldg(rowptr + T.n_rp + u + 1);
+        if (!IMPLICIT) {
+            e0 += chunk * kChunkNbrs;
+            e1 = min(e1, e0 + kChunkNbrs);
+        }
         const uint32_t la = a1 - a0;
-        const uint32_t* __restrict__ A = col + T.col_ix + a0;
-        const uint32_t* __restrict__ Bc = col + T.col_jx;
-        const uint32_t* __restrict__ vcol = col + T.col_ij;
-        const uint32_t* __restrict__ rp_jx = rowptr + T.rp_jx;
+        const uint32_t* __restrict__ A = col + T.s_col + a0;
+        const uint32_t* __restrict__ Bc = col + T.t_col;
+        const uint32_t* __restrict__ vcol = col + T.n_col;
+        const uint32_t* __restrict__ npos = T.n_pos != ~0ull ? col + T.n_pos : nullptr;
+        const uint32_t* __restrict__ rp_jx = rowptr + T.t_rp;
         const int mode = (T.wx <= kWarpBitmapBits) ? 0 : (la <= kHashMaxList ? 1 : 2);
         const uint32_t hbits = max(5, 32 - __clz(2 * la - 1));   // smallest 2^hbits >= 2 la (>= 32)
         const uint32_t hmask = (1u << hbits) - 1;
         uint32_t acc = 0;
-        unsigned long long* tvj = VM > 0 ? tv + T.cj : nullptr;
+        // per-vertex roles (R24/R25): the row vertex is LOW (LOW task) or MID (MID
+        // task), its neighbours the other one; VM 1 credits LOW only, VM >= 2 both
+        const bool row_cr = VM >= 2 || (VM == 1 && T.dir == kDirLow);
+        unsigned long long* tvj = (VM >= 2 || (VM == 1 && T.dir == kDirMid)) ? tv + T.c_nbr : nullptr;
         unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
         VCnt vc{vcnt, vpre, tvx, false};
         PROF_MARK(0);
-        if (T.bm_jx != ~0ull && 8 * la <= (T.bm_words > kDenseRowWideW ? kDenseRowMulWide : kDenseRowMul) * T.bm_words) {
-            acc = probe_dense_row<VM>(vcol, e0, e1, A, la, bitmap + T.bm_jx, T.bm_words, lane, tvj, tvx);
+        if (T.t_bm != ~0ull && 8 * la <= (T.bm_words > kDenseRowWideW ? kDenseRowMulWide : kDenseRowMul) * T.bm_words) {
+            acc = probe_dense_row<VM>(vcol, e0, e1, A, la, bitmap + T.t_bm, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);
         } else if (mode == 0) {
@@ -681,14 +702,14 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             }
             PROF_MARK(2);
             PROF_CNT(17);
-            if (T.bm_jx != ~0ull) {
-                const uint32_t* BM = bitmap + T.bm_jx;
+            if (T.t_bm != ~0ull) {
+                const uint32_t* BM = bitmap + T.t_bm;
                 const uint32_t W = T.bm_words;
-                if (W <= 32) acc = intersect_row<0, 1, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
-                else if (W <= 128) acc = intersect_row<0, 4, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
-                else acc = intersect_row<0, 0, VM>(vcol, e0, e1, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                if (W <= 32) acc = IROW(0, 1, vcol, e0, e1, npos, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else if (W <= 128) acc = IROW(0, 4, vcol, e0, e1, npos, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                else acc = IROW(0, 0, vcol, e0, e1, npos, rp_jx, Bc, BM, W, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             } else {
-                acc = intersect_row<0, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
+                acc = IROW(0, 0, vcol, e0, e1, npos, rp_jx, Bc, nullptr, 0, S, scratch, 0, 0, A, la, lane, tvj, vc PROF_PASS);
             }
             __syncwarp();
             if (VM >= 3 && vc.on) {   // flush the row's w counters: one atomic per distinct w
@@ -728,9 +749,9 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             PROF_MARK(2);
             PROF_CNT(18);
             if (filt)
-                acc = intersect_row<3, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+                acc = IROW(3, 0, vcol, e0, e1, npos, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
             else
-                acc = intersect_row<1, 0, VM>(vcol, e0, e1, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
+                acc = IROW(1, 0, vcol, e0, e1, npos, rp_jx, Bc, nullptr, 0, S, scratch, hbits, hmask, A, la, lane, tvj, vc PROF_PASS);
             if (filt) {
                 __syncwarp();
                 for (uint32_t k = lane; k < la; k += 32) S[kFilterSlots + (filter_bit(__ldg(A + k)) >> 5)] = 0u;
@@ -749,10 +770,10 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         } else {
             for (uint32_t e = e0; e < e1; ++e) {
                 const uint32_t v = __ldg(vcol + e);
-                const uint32_t b0 = __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
+                const uint32_t b0 = npos ? __ldg(npos + e) + 1 : __ldg(rp_jx + v), b1 = __ldg(rp_jx + v + 1);
                 if (b1 > b0) {
                     const uint32_t c = warp_intersect<(VM >= 3)>(A, la, Bc + b0, b1 - b0, lane, tvx);
-                    if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
+                    if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
                     acc += c;
                 }
             }
@@ -770,7 +791,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
             acc_t = 0;
         }
         acc_t += sum;
-        if (VM >= 1 && lane == 0 && sum) atomicAdd(tv + T.ci + u, (unsigned long long)sum);
+        if (VM >= 1 && row_cr && lane == 0 && sum) atomicAdd(tv + T.c_row + u, (unsigned long long)sum);
         if (TIMED && lane == 0) atomicAdd(&cyc[t], (unsigned long long)(clock64() - c0));
         PROF_MARK(7);
     }
@@ -818,6 +839,72 @@ constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
 #endif
 constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
 
+// The list branch of a light row: for each neighbour v (vcol[e0..e1)) its streamed
+// list Bc[b0..b1) -- from rowptr, or (POS: MID tasks with x == j) from after the
+// row vertex, npos[e] + 1 -- is scanned against the held ids a[] (<= kLightScan
+// ids) or binary-searched once per held id.  The next neighbour and its bounds are
+// loaded while the current list is scanned (PGABB_LIGHT_VPIPE).
+template <int VM, bool POS>
+__device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
+                                                const uint32_t* __restrict__ vcol, const uint32_t* __restrict__ npos,
+                                                uint64_t rp_jx, const uint32_t* __restrict__ Bc, uint32_t e0,
+                                                uint32_t e1, const uint32_t (&a)[kLightLa], uint32_t la,
+                                                unsigned long long* __restrict__ tvj,
+                                                unsigned long long* __restrict__ tvx) {
+    uint32_t acc = 0;
+    uint32_t vn = 0, bn0 = 0, bn1 = 0;
+    if (kLightVPipe) {
+        vn = __ldg(vcol + e0);
+        bn0 = POS ? __ldg(npos + e0) + 1 : __ldg(rowptr + rp_jx + vn);
+        bn1 = __ldg(rowptr + rp_jx + vn + 1);
+    }
+    for (uint32_t e = e0; e < e1; ++e) {
+        uint32_t v, b0, b1;
+        if (kLightVPipe) {
+            v = vn;
+            b0 = bn0;
+            b1 = bn1;
+            if (e + 1 < e1) {
+                vn = __ldg(vcol + e + 1);
+                bn0 = POS ? __ldg(npos + e + 1) + 1 : __ldg(rowptr + rp_jx + vn);
+                bn1 = __ldg(rowptr + rp_jx + vn + 1);
+            }
+        } else {
+            v = __ldg(vcol + e);
+            b0 = POS ? __ldg(npos + e) + 1 : __ldg(rowptr + rp_jx + v);
+            b1 = __ldg(rowptr + rp_jx + v + 1);
+        }
+        const uint32_t lb = b1 - b0;
+        uint32_t c = 0;
+        if (lb <= kLightScan) {
+            for (uint32_t q = b0; q < b1; ++q) {
+                const uint32_t x = __ldg(Bc + q);
+                uint32_t hit = 0;
+#pragma unroll
+                for (int k = 0; k < (int)kLightLa; ++k) hit |= (x == a[k]);
+                if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
+                c += hit;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < (int)kLightLa; ++k)
+                if (k < (int)la) {
+                    uint32_t lo = b0, hi = b1;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
+                    }
+                    const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
+                    if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
+                    c += hit;
+                }
+        }
+        acc += c;
+        if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
+    }
+    return acc;
+}
+
 // IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
 // wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
 // it is light by k_row_flags's predicate (the heavy kernel skips exactly those).
@@ -851,16 +938,17 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
             t = wp[lo].task;
             u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
             const TaskDev& Tq = tasks[t];
-            a0 = __ldg(rowptr + Tq.rp_ix + u);
-            la = __ldg(rowptr + Tq.rp_ix + u + 1) - a0;
-            e0 = __ldg(rowptr + Tq.rp_ij + u);
-            e1 = __ldg(rowptr + Tq.rp_ij + u + 1);
+            a0 = __ldg(rowptr + Tq.s_rp + u);
+            la = __ldg(rowptr + Tq.s_rp + u + 1) - a0;
+            e0 = __ldg(rowptr + Tq.n_rp + u);
+            e1 = __ldg(rowptr + Tq.n_rp + u + 1);
             if (la == 0 || e1 == e0 || la > kLightLa || e1 - e0 > kLightLe) continue;
-            if (Tq.bm_jx == ~0ull) {
+            if (Tq.t_bm == ~0ull) {
                 uint32_t work = 0;
                 for (uint32_t e = e0; e < e1; ++e) {
-                    const uint32_t v = __ldg(col + Tq.col_ij + e);
-                    work += light_pair_loads(la, __ldg(rowptr + Tq.rp_jx + v + 1) - __ldg(rowptr + Tq.rp_jx + v));
+                    const uint32_t v = __ldg(col + Tq.n_col + e);
+                    const uint32_t b0 = Tq.n_pos != ~0ull ? __ldg(col + Tq.n_pos + e) + 1 : __ldg(rowptr + Tq.t_rp + v);
+                    work += light_pair_loads(la, __ldg(rowptr + Tq.t_rp + v + 1) - b0);
                 }
                 if (work > kLightWork) continue;   // a heavy row: the warp kernel's
             }
@@ -887,13 +975,16 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
             cyc_t = 0;
         }
         const long long c0 = TIMED ? clock64() : 0;
+        // kernel roles (TaskDev, R25): u the row vertex, a[] its held list, the
+        // neighbours' streamed lists from t_col (MID, x == j: after the row vertex)
         const TaskDev& T = tasks[t];
-        const uint64_t col_ij = T.col_ij, bm_jx = T.bm_jx;
-        const uint32_t* __restrict__ A = col + T.col_ix + a0;
+        const uint64_t col_ij = T.n_col, bm_jx = T.t_bm, npos = T.n_pos;
+        const uint32_t* __restrict__ A = col + T.s_col + a0;
         uint32_t a[kLightLa];
 #pragma unroll
         for (int k = 0; k < (int)kLightLa; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
-        unsigned long long* tvj = VM > 0 ? tv + T.cj : nullptr;
+        const bool row_cr = VM >= 2 || (VM == 1 && T.dir == kDirLow);
+        unsigned long long* tvj = (VM >= 2 || (VM == 1 && T.dir == kDirMid)) ? tv + T.c_nbr : nullptr;
         unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
         uint32_t acc = 0;
         if (bm_jx != ~0ull) {
@@ -911,66 +1002,17 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                         c += hit;
                     }
                 acc += c;
-                if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
+                if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
             }
+        } else if (npos != ~0ull) {
+            acc = light_lists<VM, true>(col, rowptr, col + col_ij, col + npos, T.t_rp, col + T.t_col, e0, e1, a, la,
+                                        tvj, tvx);
         } else {
-            const uint64_t rp_jx = T.rp_jx;
-            const uint32_t* __restrict__ Bc = col + T.col_jx;
-            // software pipeline (PGABB_LIGHT_VPIPE): the next v and its list bounds are
-            // loaded while the current list is scanned
-            uint32_t vn = 0, bn0 = 0, bn1 = 0;
-            if (kLightVPipe) {
-                vn = __ldg(col + col_ij + e0);
-                bn0 = __ldg(rowptr + rp_jx + vn);
-                bn1 = __ldg(rowptr + rp_jx + vn + 1);
-            }
-            for (uint32_t e = e0; e < e1; ++e) {
-                uint32_t v, b0, b1;
-                if (kLightVPipe) {
-                    v = vn;
-                    b0 = bn0;
-                    b1 = bn1;
-                    if (e + 1 < e1) {
-                        vn = __ldg(col + col_ij + e + 1);
-                        bn0 = __ldg(rowptr + rp_jx + vn);
-                        bn1 = __ldg(rowptr + rp_jx + vn + 1);
-                    }
-                } else {
-                    v = __ldg(col + col_ij + e);
-                    b0 = __ldg(rowptr + rp_jx + v);
-                    b1 = __ldg(rowptr + rp_jx + v + 1);
-                }
-                const uint32_t lb = b1 - b0;
-                uint32_t c = 0;
-                if (lb <= kLightScan) {
-                    for (uint32_t q = b0; q < b1; ++q) {
-                        const uint32_t x = __ldg(Bc + q);
-                        uint32_t hit = 0;
-#pragma unroll
-                        for (int k = 0; k < (int)kLightLa; ++k) hit |= (x == a[k]);
-                        if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
-                        c += hit;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < (int)kLightLa; ++k)
-                        if (k < (int)la) {
-                            uint32_t lo = b0, hi = b1;
-                            while (lo < hi) {
-                                const uint32_t mid = (lo + hi) >> 1;
-                                if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
-                            }
-                            const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
-                            if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
-                            c += hit;
-                        }
-                }
-                acc += c;
-                if (VM >= 2 && c) atomicAdd(tvj + v, (unsigned long long)c);
-            }
+            acc = light_lists<VM, false>(col, rowptr, col + col_ij, nullptr, T.t_rp, col + T.t_col, e0, e1, a, la,
+                                         tvj, tvx);
         }
         acc_t += acc;
-        if (VM >= 1 && acc) atomicAdd(tv + T.ci + u, (unsigned long long)acc);
+        if (VM >= 1 && row_cr && acc) atomicAdd(tv + T.c_row + u, (unsigned long long)acc);
         if (TIMED) cyc_t += (unsigned long long)(clock64() - c0);
     }
     }

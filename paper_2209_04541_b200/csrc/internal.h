@@ -103,57 +103,89 @@ struct BlockInfo {
     uint32_t present = 0;   // nnz > 0 (rowptr stored)
     uint64_t bm_off = ~0ull; // dense copy: first word in the bitmap pool (~0: none)
     uint32_t bm_words = 0;   // words per bitmap row = ceil(width of column part / 32)
+    // transpose (DESIGN R25, MID orientation): the same nnz entries ordered by (col v,
+    // row u) at col_off inside the tcol / tpos regions of the col pool (tcol = u,
+    // tpos = block-local position e of (u,v) in col), and ncols + 1 offsets at trp_off
+    // in the rowptr pool (present blocks only, handles built with the transposes)
+    uint64_t trp_off = 0;
+    uint32_t ncols = 0;      // cut_{j+1} - cut_j
 };
+
+// Task orientation (DESIGN R25).  LOW (Listing 5's own loop order): per row u of
+// part i hold A_ix[u] and stream A_jx[v] for every v in A_ij[u].  MID: per row v
+// of part j hold A_jx[v] and stream, for every u with (u,v) in A_ij, the ids
+// w > v of A_ix[u] -- all of it when x > j, the suffix after v when x == j.
+constexpr uint32_t kDirLow = 0, kDirMid = 1;
 
 struct Task {
     uint32_t i, j, x;
-    uint64_t cost = 0;       // S7: sum_{(u,v) in A_ij} (|A_ix[u]| + |A_jx[v]|)
-    uint64_t alg_bytes = 0;  // staged model (DESIGN R19): rows u with A_ij[u], A_ix[u] non-empty,
+    uint32_t dir = kDirLow;  // orientation (R25)
+    uint64_t cost = 0;       // S7 cost in the task's orientation (cost_low or cost_mid)
+    uint64_t alg_bytes = 0;  // staged-model bytes in the task's orientation (alg_low or alg_mid)
+    uint64_t cost_low = 0;   // R17: sum_{(u,v) in A_ij} (|A_ix[u]| + |A_jx[v]|)
+    uint64_t alg_low = 0;    // R19: rows u with A_ij[u], A_ix[u] non-empty,
                              // 4*(|A_ix[u]| + sum_v |A_jx[v]|) + 12*|A_ij[u]|
+    uint64_t cost_mid = 0;   // R25: sum over rows v with a non-empty column of A_ij of
+                             // |A_jx[v]| + sum_u |{w in A_ix[u] : w > v}|
+    uint64_t alg_mid = 0;    // R25: rows v with A_jx[v] and column v non-empty,
+                             // 4*(|A_jx[v]| + sum_u |{w > v}|) + 12 per u
+    uint64_t s_low = 0, s_mid = 0;   // ids streamed by each orientation (R25 auto choice)
 };
 
 struct Piece {
     uint32_t task;
-    uint32_t r0, r1;         // local rows of part i
+    uint32_t r0, r1;         // local rows of part i (LOW task) or of part j (MID task)
     uint64_t cost;           // scheduling weight (S7 cost range, or the task weight's share, R22)
     int32_t owner;
     uint64_t rcost = 0;      // S7 row-cost range of the piece (for the bytes attribution)
 };
 
-// Work-list entry for the intersection kernels (one per owned piece).
+// One owned piece of this rank (host work list).
 struct PieceDev {
-    uint64_t gstart;         // first position in this rank's flattened edge space
-    uint64_t col_ij, rp_ij;  // pool offsets of A_ij
-    uint64_t col_ix, rp_ix;  // pool offsets of A_ix
-    uint64_t col_jx, rp_jx;  // pool offsets of A_jx
-    uint32_t r0, r1;         // local row range of the piece
-    uint32_t e0, e1;         // edge range (block-local) = rowptr_ij[r0], rowptr_ij[r1]
-    uint32_t task;
-    uint32_t pad;
+    uint64_t gstart;         // first position in this rank's flattened neighbour space
+    uint32_t r0, r1;         // local row range of the piece (rows of the task's orientation)
+    uint32_t e0, e1;         // neighbour range = nbr rowptr[r0], nbr rowptr[r1] (block-local)
+    uint32_t task, dir;
 };
 
-// Per-task descriptor read by the intersection kernel.
+// Per-task descriptor read by the intersection kernels, in kernel ROLES (R25):
+//   row r     the item's vertex: u of part i (LOW) / v of part j (MID)
+//   held S    the row's list: A_ix[u] (LOW) / A_jx[v] (MID)
+//   nbr       the row's neighbours r': A_ij[u] = the v's (LOW) / column v of A_ij =
+//             the u's (MID, the transpose)
+//   streamed  each neighbour's list: A_jx[v] (LOW) / A_ix[u] from its first id > v
+//             (MID: the suffix after position e of (u,v) in A_ij when x == j)
+// All offsets are words into the col / rowptr / bitmap pools (or a wave's arena).
 struct TaskDev {
-    uint64_t col_ij, rp_ij;  // pool offsets of A_ij
-    uint64_t col_ix, rp_ix;  // pool offsets of A_ix
-    uint64_t col_jx, rp_jx;  // pool offsets of A_jx
-    uint64_t bm_jx;          // bitmap-pool offset of dense A_jx rows, ~0 if A_jx is list-only
+    uint64_t s_col, s_rp;    // held block (col, rowptr)
+    uint64_t n_col, n_rp;    // neighbour ids (col pool: A_ij's cols or the transpose's tcol) + rowptr
+    uint64_t n_pos;          // MID with x == j: the transpose's tpos (suffix start - 1), else ~0
+    uint64_t t_col, t_rp;    // streamed block (col, rowptr)
+    uint64_t t_bm;           // bitmap copy of the streamed block, ~0 if list-only
     uint32_t wx;             // width of column part x (bits of a bitmap over it)
-    uint32_t bm_words;       // words per dense row of A_jx
-    uint32_t ci, cj, cx;     // rank-space first vertex of parts i, j, x (cuts; per-vertex counts)
-    uint32_t pad;
+    uint32_t bm_words;       // words per dense row of the streamed block
+    uint32_t c_row, c_nbr, cx;   // rank-space first vertex of the row's, the neighbours' and part x
+    uint32_t dir;
 };
+static_assert(sizeof(TaskDev) == 88, "TaskDev layout");
 
 // A block gets a dense bitmap copy (rows of ceil(w/32) words) when its density is
 // at least 1/kDenseInv and its column part is narrow enough for a warp bitmap:
 // then the copy is no larger than the list form.
 constexpr uint64_t kDenseInv = 32;
 
-// A row item: (task, local row u of part i) with A_ij[u] and A_ix[u] non-empty.
-// Packed as (task << 32) | u; items are sorted by estimated work, heaviest first.
+// A heavy row item: (task, local row r, chunk c) with the row's held list and
+// neighbour list non-empty; the warp takes neighbours [c*kChunkNbrs, (c+1)*kChunkNbrs)
+// of the row (a MID hub row can have 10^5+ neighbours).  Packed as
+// task << 48 | c << 32 | r.
 constexpr uint32_t kColPad = 4;               // u32 words of padding after col pools / arenas
 constexpr uint32_t kWarpBitmapBits = 32768;   // per-warp smem bitmap: 4 KB
 constexpr uint32_t kHashMaxList = 512;        // per-warp smem hash: 1024 slots
+#ifndef PGABB_CHUNK_NBRS
+#define PGABB_CHUNK_NBRS 2048
+#endif
+constexpr uint32_t kChunkNbrs = PGABB_CHUNK_NBRS;   // neighbours per heavy item
+__host__ __device__ inline uint32_t heavy_chunks(uint32_t le) { return (le + kChunkNbrs - 1) / kChunkNbrs; }
 
 // Light rows (DESIGN R20): handled one per thread by k_tc_light, A_ix[u] held in
 // registers.  A v list of <= kLightScan ids is scanned (each id compared with all
@@ -176,7 +208,7 @@ constexpr uint32_t kLightScan = PGABB_LIGHT_SCAN;
 constexpr uint32_t kLightWork = PGABB_LIGHT_WORK;   // list loads per row
 // A light item carries its row's offsets, so the kernel starts with the lists
 // instead of a chain of descriptor / rowptr loads:
-//   x = task | |A_ix[u]| << 16 | |A_ij[u]| << 20,  y = rowptr_ix[u],  z = rowptr_ij[u],  w = u
+//   x = task | |S| << 16 | |nbr| << 20,  y = held rowptr[r],  z = nbr rowptr[r],  w = r
 // (task < 2^16: p <= 64 gives at most C(66,3) = 45760 tasks).
 constexpr uint32_t kLightTaskBits = 16;
 static_assert(kLightLa < 16 && kLightLe < 4096, "light item bit fields");
@@ -201,6 +233,11 @@ struct StagedBlock {        // one H2D copy: pool range -> arena offset (u32 wor
     int pool;               // 0 col, 1 rowptr, 2 bitmap (host pools); 3 = the other arena (device copy)
 };
 
+// Per-block arrays a task reads, by kind (S9 residency and streaming): the col
+// pool's three regions (cols, transposed u's, transposed positions), the rowptr
+// pool's two (rowptr, transposed rowptr) and the bitmap pool.
+enum BlockPart { kPartCol = 0, kPartRp = 1, kPartBm = 2, kPartTCol = 3, kPartTPos = 4, kPartTRp = 5 };
+
 struct Wave {
     std::vector<StagedBlock> copies;
     uint64_t words = 0;         // arena words used
@@ -221,6 +258,9 @@ struct pgabb_blocks_s {
     int32_t rank = 0, world_size = 1;
     uint32_t residency = PGABB_RESIDENT_DEVICE;
     uint32_t reverse_order = 0;                 // S2 ranks reversed (DESIGN R24)
+    uint32_t orient = 0;                        // R25: 0 auto, 1 all LOW, 2 all MID
+    bool has_t = false;                         // transposes built (orient != 1)
+    uint64_t tcol_base = 0, tpos_base = 0;      // word offsets of the col pool's transpose regions
     uint64_t budget = 0;
     uint64_t wedges = 0;
 
@@ -246,7 +286,6 @@ struct pgabb_blocks_s {
     // this rank's work list
     std::vector<pgabb::PieceDev> work;
     uint64_t work_edges = 0;
-    pgabb::DBuf<pgabb::PieceDev> d_work;
     pgabb::DBuf<pgabb::TaskDev> d_tasks;             // ntasks descriptors
     pgabb::DBuf<unsigned long long> d_items;         // heavy row items (warp per row)
     uint64_t n_items = 0;
@@ -291,6 +330,11 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
 void plan_pieces(pgabb_blocks_s* h);
 void upload_work(pgabb_blocks_s* h);
 void plan_waves(pgabb_blocks_s* h);
+// the blocks and parts a task reads in its orientation (S9), and their word ranges
+struct PartRef { uint32_t block; int part; };
+int task_parts(const pgabb_blocks_s* h, const Task& T, PartRef out[8]);
+uint64_t part_words(const pgabb_blocks_s* h, PartRef r);
+uint64_t part_src(const pgabb_blocks_s* h, PartRef r, int* pool);   // word offset in host pool *pool
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
                          unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr,
                          int vm = 3);

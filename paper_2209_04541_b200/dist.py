@@ -87,7 +87,7 @@ def build_blocks_balanced(n, src, dst, p=0, cut_rule=0, group=None, **kw):
         return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, **kw)
     ns = None
     if rank == 0:
-        with build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev) as b1:
+        with build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, orient=kw.get("orient", "auto")) as b1:
             ns = b1.task_times()
     w = broadcast_weights(ns, group)
     b = build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,

@@ -170,12 +170,13 @@ SMALL = [
 ]
 
 
+@pytest.mark.parametrize("orient", [0, 1, 2])   # R25: auto, low, mid
 @pytest.mark.parametrize("name,mk", SMALL)
 @pytest.mark.parametrize("p,rule", [(1, 0), (2, 0), (3, 1), (5, 0), (8, 1)])
-def test_steps_parity(name, mk, p, rule):
+def test_steps_parity(name, mk, p, rule, orient):
     g = mk()
-    P = ob.Plan(*g, p=p, rule=rule)
-    with pg.build_blocks(*g, p=p, cut_rule=rule) as b:
+    P = ob.Plan(*g, p=p, rule=rule, orient=orient)
+    with pg.build_blocks(*g, p=p, cut_rule=rule, orient=orient) as b:
         st = b.stats()
         assert st["m_edges"] == len(P.E)
         assert st["p"] == P.p
@@ -190,24 +191,29 @@ def test_steps_parity(name, mk, p, rule):
         assert [tuple(map(int, t)) for t in ijx] == P.tasks
         assert list(map(int, cost)) == P.costs
         assert list(map(int, alg)) == P.alg_bytes
+        dirs, s_low, s_mid = b.task_orient()                                 # R25
+        assert list(map(int, dirs)) == P.dirs
+        if orient != 1:
+            assert [(int(a), int(c)) for a, c in zip(s_low, s_mid)] == [ob.task_streams(P.B, t) for t in P.tasks]
         assert st["wedges"] == ob.wedges_dag(g[0], P.D)
         T, tc = b.triangle_count(task_counts=True)                           # S10, S11
         assert list(map(int, tc)) == P.task_counts()
         assert T == oracle.count(*g)
 
 
+@pytest.mark.parametrize("orient", [0, 1, 2])
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_pieces_lpt_and_rank_sum(G):
+def test_pieces_lpt_and_rank_sum(G, orient):
     g = gen.rmat(10, 16, seed=21)
-    P = ob.Plan(*g, p=4, G=G)
+    P = ob.Plan(*g, p=4, G=G, orient=orient)
     total = 0
     for r in range(G):   # logical-rank simulation on one GPU
-        with pg.build_blocks(*g, p=4, rank=r, world_size=G) as b:
+        with pg.build_blocks(*g, p=4, rank=r, world_size=G, orient=orient) as b:
             pcs, owner = b.pieces()
             assert pcs == P.pieces                                           # S8 pieces
             assert owner == P.owner                                          # S8 LPT
             T_r, tc = b.triangle_count(task_counts=True)
-            want = sum(ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2])
+            want = sum(ob.piece_count(P.B, P.tasks[pc[0]], pc[1], pc[2], P.dirs[pc[0]])
                        for pc, o in zip(P.pieces, P.owner) if o == r)
             assert T_r == want
             total += T_r
@@ -222,10 +228,10 @@ def test_weighted_pieces_and_rank_sum(G):
         nt = b1.ntasks
     rng = np.random.default_rng(G)
     w = rng.integers(0, 10 ** 9, nt).astype(np.uint64)
-    P = ob.Plan(*g, p=5, G=G, weights=[int(x) for x in w])
+    P = ob.Plan(*g, p=5, G=G, weights=[int(x) for x in w], orient=0)
     total = 0
     for r in range(G):
-        with pg.build_blocks(*g, p=5, rank=r, world_size=G, task_weights=w) as b:
+        with pg.build_blocks(*g, p=5, rank=r, world_size=G, task_weights=w, orient=0) as b:
             pcs, owner = b.pieces()
             assert pcs == P.pieces and owner == P.owner
             total += b.triangle_count()

@@ -159,7 +159,7 @@ def test_two_pass_vertex_triangles():
 
 def test_reverse_order_steps_parity():
     g = gen.rmat(9, 16, seed=44)
-    P = ob.Plan(*g, p=3, reverse=True)
+    P = ob.Plan(*g, p=3, reverse=True, orient=0)
     with pg.build_blocks(*g, p=3, reverse_order=True) as b:
         assert (b.rank() == P.rank).all()
         assert list(b.cuts()) == list(P.cuts)

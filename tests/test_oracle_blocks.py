@@ -347,7 +347,7 @@ def test_auto_orientation_picks_fewer_streams():
     assert ob.MID in P.dirs
     for t, d in zip(P.tasks, P.dirs):
         s_low, s_mid = ob.task_streams(P.B, t)
-        assert d == (ob.MID if s_mid < s_low else ob.LOW)
+        assert d == (ob.MID if 4 * s_mid < 3 * s_low else ob.LOW)
 
 
 @pytest.mark.parametrize("orient", [0, 2])
