@@ -35,9 +35,10 @@ CONFIGS = {
     "c1": Config("c1", "R-MAT scale 10, edge factor 16, 2x2 blocks", 2, "rmat", (10, 16, 1)),
     "c2": Config("c2", "R-MAT scale 20, edge factor 16, 8x8 blocks", 8, "rmat", (20, 16, 1)),
     "c3": Config("c3", "Erdos-Renyi n=2^24, avg degree 32, 16x16 blocks", 16, "er", (1 << 24, 32, 1)),
-    # p = 4: measured on B200 (count 1.8 / 2.1 / 2.5 / 3.1 ms at p = 4 / 6 / 8 / 16): a
-    # low-degree grid gains nothing from narrow parts and pays per (edge, part) pair
-    "c4": Config("c4", "grid 8192^2 + 10% diagonals (road-like), n=2^26, 4x4 blocks", 4, "grid",
+    # p = 1: measured on B200 (round 2: count 1.09 / 1.45 / 1.65 / 1.84 / 2.09 ms at
+    # p = 1 / 2 / 3 / 4 / 6): a low-degree grid gains nothing from narrow parts and pays
+    # per (edge, part) pair
+    "c4": Config("c4", "grid 8192^2 + 10% diagonals (road-like), n=2^26, 1x1 block", 1, "grid",
                  (8192, 0.1, 1)),
     # profiling stand-in for c5 (same generator and p at 1/4 of the vertices; ncu-sized)
     "c5s": Config("c5s", "R-MAT scale 24, edge factor 32, 16x16 blocks", 16, "rmat", (24, 32, 1)),

@@ -77,7 +77,10 @@ enum {
 typedef struct {
     uint32_t p;                 /* parts per dimension; 0 = 8; clamped to [1, n] */
     uint32_t cut_rule;          /* 0 = balance estimated work w(v) = d+(v) + d-(v)d+(v)
-                                   1 = balance DAG out-degree w(v) = d+(v)   (DESIGN R7) */
+                                   1 = balance DAG out-degree w(v) = d+(v)
+                                   2 = balance degree w(v) = d+(v) + d-(v)
+                                   3 = balance estimated MID work w(v) = d+(v) + C(d+(v), 2)
+                                   (DESIGN R7, R25) */
     int32_t device;             /* CUDA ordinal, -1 = current device */
     uint32_t inputs_on_device;  /* 1: src/dst are device pointers on `device`; the build
                                    synchronizes the device before reading them, so tuples

@@ -66,6 +66,10 @@ def cut_weights(n: int, D: np.ndarray, rule: int) -> np.ndarray:
         return dplus + dminus * dplus
     if rule == 1:        # DAG out-degree
         return dplus
+    if rule == 2:        # degree
+        return dplus + dminus
+    if rule == 3:        # estimated MID work (R25): d+ + C(d+, 2), the ids streamed for u's list
+        return np.array([int(x) + int(x) * (int(x) - 1) // 2 for x in dplus], dtype=object)
     raise ValueError("cut rule")
 
 
@@ -231,16 +235,23 @@ def task_streams(B, t):
     return s_low, s_mid
 
 
+MID_SAVING = 2
+
+
 def orientation(B, t, orient=0) -> int:
-    """orient 1 = LOW, 2 = MID, 0 = auto: MID iff it streams at most 3/4 of LOW's
-    ids (4 S_mid < 3 S_low; a MID row reads its neighbours from the transpose, and
-    near-equal streams measured faster in LOW -- ER, DESIGN R25)."""
+    """orient 1 = LOW, 2 = MID, 0 = auto: MID iff it streams (a) more than
+    MID_SAVING fewer ids per visit (per edge of A_ij), S_mid + 2 nnz(A_ij) < S_low,
+    and (b) at most 3/4 of LOW's ids, 4 S_mid < 3 S_low.  A MID visit first reads
+    the transpose's u (and suffix position), which short lists do not repay, and
+    LOW streams hub lists as bitmap words, which a small saving does not beat
+    (DESIGN R25: ER, grid and R-MAT hub tasks measured faster in LOW)."""
     if orient == 1:
         return LOW
     if orient == 2:
         return MID
     s_low, s_mid = task_streams(B, t)
-    return MID if 4 * s_mid < 3 * s_low else LOW
+    visits = int(B[(t[0], t[1])][1].size)
+    return MID if s_mid + MID_SAVING * visits < s_low and 4 * s_mid < 3 * s_low else LOW
 
 
 def row_costs_mid(B, t) -> np.ndarray:

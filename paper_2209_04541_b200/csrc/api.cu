@@ -112,7 +112,7 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         pgabb_build_opts_t o;
         pgabb_default_build_opts(&o);
         if (opts_in) o = *opts_in;
-        if (o.cut_rule > 1) fail(PGABB_EINVAL, "cut_rule must be 0 or 1");
+        if (o.cut_rule > 3) fail(PGABB_EINVAL, "cut_rule must be 0, 1, 2 or 3");
         if (o.residency > PGABB_RESIDENT_HOST) fail(PGABB_EINVAL, "bad residency");
         if (o.world_size < 1) o.world_size = 1;
         if (o.rank < 0 || o.rank >= o.world_size) fail(PGABB_EINVAL, "rank outside [0, world_size)");

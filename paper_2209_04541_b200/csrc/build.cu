@@ -28,6 +28,10 @@ namespace pgabb {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef PGABB_LIGHT_SORT_WINDOW
+#define PGABB_LIGHT_SORT_WINDOW 4096
+#endif
+constexpr uint32_t kLightSortWindow = PGABB_LIGHT_SORT_WINDOW;   // light items re-ordered by work within it
 
 inline unsigned grid_for(uint64_t work, int threads = kThreads) {
     uint64_t g = (work + threads - 1) / threads;
@@ -41,6 +45,8 @@ inline int bits_for(uint64_t x) {
     while (b < 64 && (x >> b) != 0) ++b;
     return b;
 }
+
+constexpr uint64_t kMidSaving = 2;   // R25 auto: saved streamed ids per visit needed for MID
 
 struct CutsArg {
     uint32_t c[kMaxParts + 1];
@@ -126,7 +132,9 @@ __global__ void k_cut_weights(const uint32_t* dplus, const uint32_t* dminus, uin
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x) {
         unsigned long long dp = dplus[k], dm = dminus[k];
-        w[k] = rule == 0 ? dp + dm * dp : dp;
+        // R7: 0 estimated LOW work d+ + d-d+, 1 out-degree d+, 2 degree d+ + d-,
+        // 3 estimated MID work d+ + C(d+, 2) (R25: the ids streamed for u's lists)
+        w[k] = rule == 0 ? dp + dm * dp : rule == 1 ? dp : rule == 2 ? dp + dm : dp + dp * (dp - (dp > 0)) / 2;
         acc += dm * dp;
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -499,9 +507,13 @@ __global__ void k_row_emit(PieceDev w, const uint32_t* nchunks, const uint32_t* 
             out[pos[k] + c] = ((unsigned long long)w.task << 48) | ((unsigned long long)c << 32) | (w.r0 + (uint32_t)k);
 }
 
-// Light items of one owned piece (16 bytes each, see internal.h).
+// Light items of one owned piece (16 bytes each, see internal.h), and each item's
+// sort key: its window of kLightSortWindow items (row order, for L2 locality) then
+// its work (neighbour count + list loads), so that a warp's 32 lanes (32
+// consecutive items) get items of similar work -- the loops of the light kernel
+// run as long as the warp's longest item.
 __global__ void k_light_emit(PieceDev w, const TaskDev* tasks, const uint32_t* flags, const uint32_t* pos,
-                             const uint32_t* rowptr, uint4* out) {
+                             const uint32_t* col, const uint32_t* rowptr, uint4* out, uint32_t* key) {
     const TaskDev T = tasks[w.task];
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nr;
@@ -511,6 +523,10 @@ __global__ void k_light_emit(PieceDev w, const TaskDev* tasks, const uint32_t* f
             const uint32_t a0 = rowptr[T.s_rp + r], la = rowptr[T.s_rp + r + 1] - a0;
             const uint32_t e0 = rowptr[T.n_rp + r], le = rowptr[T.n_rp + r + 1] - e0;
             out[pos[k]] = make_uint4(w.task | (la << kLightTaskBits) | (le << (kLightTaskBits + 4)), a0, e0, r);
+            uint32_t work = le;
+            for (uint32_t e = e0; e < e0 + le; ++e)
+                work += T.t_bm != ~0ull ? la : light_pair_loads(la, streamed_len(T, col, rowptr, e));
+            key[pos[k]] = (pos[k] / kLightSortWindow) << 8 | min(work, 255u);
         }
 }
 
@@ -917,11 +933,16 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
             T.alg_mid = am[t];
             T.s_low = sl[t];
             T.s_mid = sm[t];
-            // R25: orient 1 -> LOW, 2 -> MID, 0 (auto) -> MID iff it streams at most 3/4
-            // of LOW's ids (near-equal streams measured faster in LOW: ER c3)
-            T.dir = !h->has_t ? kDirLow
-                    : h->orient == 2 ? kDirMid
-                                     : ((unsigned __int128)4 * sm[t] < (unsigned __int128)3 * sl[t] ? kDirMid : kDirLow);
+            // R25: orient 1 -> LOW, 2 -> MID, 0 (auto) -> MID iff it streams (a) more than
+            // kMidSaving fewer ids per visit (per edge of A_ij) -- a MID visit reads the
+            // transpose's u (and suffix position) first, which short lists do not repay
+            // (measured: ER c3, grid c4 faster in LOW) -- and (b) at most 3/4 of LOW's
+            // ids -- LOW streams hub lists as bitmap words, so a small saving is not one
+            // (measured: c2's hub tasks faster in LOW; R-MAT c2/c5 otherwise in MID)
+            const uint64_t visits = h->blocks[T.i * p + T.j].nnz;
+            const bool mid_wins = (unsigned __int128)sm[t] + (unsigned __int128)kMidSaving * visits < sl[t] &&
+                                  (unsigned __int128)4 * sm[t] < (unsigned __int128)3 * sl[t];
+            T.dir = !h->has_t ? kDirLow : h->orient == 2 ? kDirMid : (mid_wins ? kDirMid : kDirLow);
             T.cost = T.dir == kDirMid ? T.cost_mid : T.cost_low;
             T.alg_bytes = T.dir == kDirMid ? T.alg_mid : T.alg_low;
             h->cost_total += T.cost;
@@ -1347,6 +1368,15 @@ void upload_work(pgabb_blocks_s* h) {
     h->alg_light = alg_light;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
     h->d_light.alloc(std::max<uint64_t>(nlight, 1));
+    uint64_t max_light = 0;
+    for (uint64_t c : piece_light) max_light = std::max(max_light, c);
+    DBuf<uint32_t> lkey, lkey2;
+    DBuf<uint4> litem2;
+    if (max_light) {
+        lkey.alloc(max_light);
+        lkey2.alloc(max_light);
+        litem2.alloc(max_light);
+    }
     // pass 2: emit in layout order
     uint64_t base = 0, lbase = 0;
     for (size_t k : order) {
@@ -1359,9 +1389,17 @@ void upload_work(pgabb_blocks_s* h) {
             PG_LAUNCH_CHECK();
         }
         if (piece_light[k]) {
-            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_tasks.p, lf.p, lpos.p, h->d_rowptr.p,
-                                                            h->d_light.p + lbase);
+            uint4* li = h->d_light.p + lbase;
+            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_tasks.p, lf.p, lpos.p, h->d_col.p, h->d_rowptr.p,
+                                                            li, lkey.p);
             PG_LAUNCH_CHECK();
+            // the piece's light items by work (stable: rows ascending within equal work)
+            const int64_t nl = (int64_t)piece_light[k];
+            const int kb = 8 + bits_for((uint64_t)(nl - 1) / kLightSortWindow);
+            cub_call([&](void* tp, size_t& b) {
+                return cub::DeviceRadixSort::SortPairs(tp, b, lkey.p, lkey2.p, li, litem2.p, nl, 0, kb, st);
+            }, st, tmp);
+            PG_CK(cudaMemcpyAsync(li, litem2.p, (size_t)nl * sizeof(uint4), cudaMemcpyDeviceToDevice, st));
         }
         base += piece_items[k];
         lbase += piece_light[k];

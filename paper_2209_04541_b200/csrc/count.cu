@@ -844,7 +844,9 @@ constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
 // row vertex, npos[e] + 1 -- is scanned against the held ids a[] (<= kLightScan
 // ids) or binary-searched once per held id.  The next neighbour and its bounds are
 // loaded while the current list is scanned (PGABB_LIGHT_VPIPE).
-template <int VM, bool POS>
+// LA: a bound on |held| for the whole warp (1, 2, 4 or kLightLa), so a scanned id
+// is compared with LA held slots, not kLightLa (unused slots are ~0u).
+template <int VM, bool POS, int LA>
 __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
                                                 const uint32_t* __restrict__ vcol, const uint32_t* __restrict__ npos,
                                                 uint64_t rp_jx, const uint32_t* __restrict__ Bc, uint32_t e0,
@@ -881,13 +883,13 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
                 const uint32_t x = __ldg(Bc + q);
                 uint32_t hit = 0;
 #pragma unroll
-                for (int k = 0; k < (int)kLightLa; ++k) hit |= (x == a[k]);
+                for (int k = 0; k < LA; ++k) hit |= (x == a[k]);
                 if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
                 c += hit;
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < (int)kLightLa; ++k)
+            for (int k = 0; k < LA; ++k)
                 if (k < (int)la) {
                     uint32_t lo = b0, hi = b1;
                     while (lo < hi) {
@@ -1004,12 +1006,19 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
                 acc += c;
                 if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
             }
-        } else if (npos != ~0ull) {
-            acc = light_lists<VM, true>(col, rowptr, col + col_ij, col + npos, T.t_rp, col + T.t_col, e0, e1, a, la,
-                                        tvj, tvx);
         } else {
-            acc = light_lists<VM, false>(col, rowptr, col + col_ij, nullptr, T.t_rp, col + T.t_col, e0, e1, a, la,
-                                         tvj, tvx);
+            // the warp's largest held list picks the compare width (warp-uniform)
+            const uint32_t lam = __reduce_max_sync(__activemask(), la);
+#define LLISTS(P, L)                                                                                       \
+    light_lists<VM, P, L>(col, rowptr, col + col_ij, P ? col + npos : nullptr, T.t_rp, col + T.t_col, e0, e1, a, \
+                          la, tvj, tvx)
+            if (npos != ~0ull)
+                acc = lam <= 1 ? LLISTS(true, 1) : lam <= 2 ? LLISTS(true, 2) : lam <= 4 ? LLISTS(true, 4)
+                                                                                 : LLISTS(true, (int)kLightLa);
+            else
+                acc = lam <= 1 ? LLISTS(false, 1) : lam <= 2 ? LLISTS(false, 2) : lam <= 4 ? LLISTS(false, 4)
+                                                                                   : LLISTS(false, (int)kLightLa);
+#undef LLISTS
         }
         acc_t += acc;
         if (VM >= 1 && row_cr && acc) atomicAdd(tv + T.c_row + u, (unsigned long long)acc);

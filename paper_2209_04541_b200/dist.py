@@ -11,14 +11,17 @@ from __future__ import annotations
 from . import Blocks, build_blocks
 
 
-def build_blocks_for_rank(n, src, dst, p=0, cut_rule=0, residency=0, device_budget_bytes=0, group=None):
+def build_blocks_for_rank(n, src, dst, p=0, cut_rule=0, residency=0, device_budget_bytes=0, group=None,
+                          orient="auto"):
+    """This rank's handle: every rank builds the same grid from the same tuples
+    (S1-S8 are deterministic) and keeps the LPT share of pieces it owns."""
     import torch
     import torch.distributed as dist
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     ws = dist.get_world_size(group) if dist.is_initialized() else 1
     dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
     return build_blocks(n, src, dst, p=p, cut_rule=cut_rule, device=dev, rank=rank, world_size=ws,
-                        residency=residency, device_budget_bytes=device_budget_bytes)
+                        residency=residency, device_budget_bytes=device_budget_bytes, orient=orient)
 
 
 def triangle_count_allreduce(b: Blocks, out=None, group=None) -> int:

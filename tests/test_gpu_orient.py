@@ -133,7 +133,10 @@ def test_auto_picks_mid_on_rmat():
     with pg.build_blocks(*g, p=8) as b:
         d, sl, sm = b.task_orient()
         assert (d == 1).sum() > 0
-        assert all((dd == 1) == (4 * int(m) < 3 * int(l)) for dd, l, m in zip(d, sl, sm))
+        ijx, _, _ = b.tasks()
+        visits = [b.block(int(i), int(j))[1].size for i, j, _ in ijx]
+        assert all((dd == 1) == (int(m) + 2 * nv < int(l) and 4 * int(m) < 3 * int(l))
+                   for dd, l, m, nv in zip(d, sl, sm, visits))
     with pg.build_blocks(*g, p=8, orient="low") as b:
         d, sl, sm = b.task_orient()
         assert (d == 0).all() and (sm == 0).all()

@@ -67,7 +67,7 @@ def test_errors():
         pg.build_blocks(3, np.array([0], np.uint32), np.array([1], np.uint32), rank=2, world_size=2)
     assert e.value.name == "EINVAL"
     with pytest.raises(pg.PgabbError):
-        pg.build_blocks(3, np.array([0], np.uint32), np.array([1], np.uint32), cut_rule=7)
+        pg.build_blocks(3, np.array([0], np.uint32), np.array([1], np.uint32), cut_rule=4)
 
 
 # ---------------------------------------------------------------- totals vs oracle
@@ -172,7 +172,7 @@ SMALL = [
 
 @pytest.mark.parametrize("orient", [0, 1, 2])   # R25: auto, low, mid
 @pytest.mark.parametrize("name,mk", SMALL)
-@pytest.mark.parametrize("p,rule", [(1, 0), (2, 0), (3, 1), (5, 0), (8, 1)])
+@pytest.mark.parametrize("p,rule", [(1, 0), (2, 0), (3, 1), (5, 0), (8, 1), (4, 2), (6, 3)])
 def test_steps_parity(name, mk, p, rule, orient):
     g = mk()
     P = ob.Plan(*g, p=p, rule=rule, orient=orient)

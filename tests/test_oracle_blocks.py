@@ -68,10 +68,21 @@ def test_cuts_p4_hand():
     # P4: DAG (rank space) (0,2),(1,3),(2,3); d+=[1,1,1,0], d-=[0,0,1,2]
     # rule 0 weights [1,1,2,0], P=[0,1,2,4,4]: p=2 -> [0,2,4]; p=3 -> [0,2,3,4]
     # rule 1 weights [1,1,1,0], P=[0,1,2,3,3]: p=2 -> 2P>=3 -> c=2
+    # rule 2 weights deg [1,1,2,2], P=[0,1,2,4,6]: p=2 -> 2P>=6 -> c=3 -> [0,3,4]
+    # rule 3 weights d+ + C(d+,2) = [1,1,1,0] (C(1,2) = 0): as rule 1
     g = gen.path(4)
     assert list(_plan_objs(g, 2, 0)[2]) == [0, 2, 4]
     assert list(_plan_objs(g, 3, 0)[2]) == [0, 2, 3, 4]
     assert list(_plan_objs(g, 2, 1)[2]) == [0, 2, 4]
+    assert list(_plan_objs(g, 2, 2)[2]) == [0, 3, 4]
+    assert list(_plan_objs(g, 2, 3)[2]) == [0, 2, 4]
+
+
+def test_cut_weights_rules_2_3_k4():
+    # K4: d+ = [3,2,1,0], d- = [0,1,2,3]: degree 3 each; d+ + C(d+,2) = [6,3,1,0]
+    n, D, _ = _plan_objs(gen.complete(4), 1)
+    assert [int(x) for x in ob.cut_weights(n, D, 2)] == [3, 3, 3, 3]
+    assert [int(x) for x in ob.cut_weights(n, D, 3)] == [6, 3, 1, 0]
 
 
 def test_cuts_p1_and_clamp():
@@ -84,7 +95,7 @@ def test_cuts_p1_and_clamp():
 def test_cuts_balance_property():
     # prefix cuts: every part's weight <= W/p + max single weight
     g = gen.rmat(10, 16, 2)
-    for rule in (0, 1):
+    for rule in (0, 1, 2, 3):
         for p in (2, 3, 5, 8):
             n, D, c = _plan_objs(g, p, rule)
             w = np.array([int(x) for x in ob.cut_weights(n, D, rule)], dtype=np.int64)
@@ -332,7 +343,7 @@ def test_mid_costs_k4_by_hand():
     #   v=3: column {0,1,2}; |A[3]| = 0 + nothing after 3                 -> 0
     # cost 7; bytes: v=1 4*(2+2)+12, v=2 4*(1+2)+24 (v=3 holds nothing) = 64.
     # Streams: S_low = sum over edges of |A[v]| = 2+1+0+1+0+0 = 4, S_mid = C(3,2)+C(2,2) = 4:
-    # a tie, so auto keeps LOW.
+    # no saving, so auto keeps LOW.
     P = ob.Plan(*gen.complete(4), p=1, orient=2)
     t = P.tasks[0]
     assert list(ob.row_costs_mid(P.B, t)) == [0, 4, 3, 0]
@@ -347,7 +358,8 @@ def test_auto_orientation_picks_fewer_streams():
     assert ob.MID in P.dirs
     for t, d in zip(P.tasks, P.dirs):
         s_low, s_mid = ob.task_streams(P.B, t)
-        assert d == (ob.MID if 4 * s_mid < 3 * s_low else ob.LOW)
+        assert d == (ob.MID if s_mid + 2 * P.B[(t[0], t[1])][1].size < s_low and 4 * s_mid < 3 * s_low
+                     else ob.LOW)
 
 
 @pytest.mark.parametrize("orient", [0, 2])

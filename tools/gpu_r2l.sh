@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round 2: light items sorted by work + warp-uniform compare width: parity + bench lines.
+T=${1:-r2l}
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_orient.py tests/test_gpu_vertex.py -q -x -p no:cacheprovider > gpurun_out/pytest_$T.log 2>&1; tail -n 2 gpurun_out/pytest_$T.log
+summ() { python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[2], d.get('ms_per_step'), d.get('parity',{}).get('match'), [ (k['kernel'], round(k['ms'],3)) for k in d['roofline']['kernels']])" $1 "$2" 2>&1 | tail -1; }
+for c in c2 c3 c4 c5; do
+  for o in ${ORIENTS:-auto low}; do
+    timeout 900 python bench.py --config $c --orient $o --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_${c}_${o}_$T.json 2> gpurun_out/bench_${c}_${o}_$T.err
+    summ gpurun_out/bench_${c}_${o}_$T.json "$c $o"
+  done
+done
+for p in 12; do
+  timeout 900 python bench.py --config c3 --p $p --orient low --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c3_p${p}_$T.json 2> gpurun_out/bench_c3_p${p}_$T.err
+  summ gpurun_out/bench_c3_p${p}_$T.json "c3 p=$p low"
+done
