@@ -60,7 +60,7 @@ typedef enum {
     PGABB_EINVAL = 1,   /* bad argument: vertex id >= n, NULL pointer, bad option */
     PGABB_ENOMEM = 2,   /* device or pinned-host allocation failed */
     PGABB_ECUDA = 3,    /* CUDA error (incl. no device) */
-    PGABB_ERANGE = 4,   /* size outside the supported range (|E| >= 2^32, n >= 2^31) */
+    PGABB_ERANGE = 4,   /* size outside the supported range (a block with >= 2^32 edges) */
     PGABB_EBUDGET = 5   /* host-resident handle: one task's 3 blocks exceed the budget */
 } pgabb_status_t;
 
@@ -128,7 +128,10 @@ PGABB_API void pgabb_default_build_opts(pgabb_build_opts_t* opts);
 /*
  * S1-S8.  n: number of vertex ids; m: number of tuples; src[k], dst[k] < n are
  * the k-th tuple (uint32, host memory unless opts->inputs_on_device).  m == 0 is
- * valid (an empty graph, count 0).  Requires n < 2^31 and |E| < 2^32.
+ * valid (an empty graph, count 0).  Ids are uint32 (n <= 2^32 - 1) and |E| is 64-bit;
+ * the only size limit is that no single block A_ij may hold 2^32 or more edges
+ * (block-local offsets are uint32: ERANGE, pick a larger p), besides device memory
+ * for the build (about 28 bytes per edge at the peak).
  * opts == NULL means defaults.  On success *out receives a new handle.
  * Errors: EINVAL (id >= n, src/dst NULL with m > 0, out NULL, bad rank/p/rule),
  *         ERANGE, ENOMEM, ECUDA.
@@ -161,6 +164,9 @@ typedef struct {
 #define PGABB_ROLE_HIGH 16u
 /* pgabb_vertex_triangles with PGABB_OUT_DEVICE: ADD this pass's t(v) into tv instead
    of overwriting it (the second pass of the two-pass route) */
+/* pgabb_triangle_count / pgabb_vertex_triangles on a streaming handle: record CUDA
+   events around every wave's copies and kernels (read with pgabb_get_wave_trace) */
+#define PGABB_COUNT_TRACE 64u
 #define PGABB_OUT_ACCUMULATE 32u     /* pgabb_vertex_triangles / pgabb_local_clustering: the
                                    tv and cc arrays are DEVICE pointers on the handle's
                                    device (stream-ordered on opts->cuda_stream) */
@@ -288,6 +294,14 @@ PGABB_API pgabb_status_t pgabb_get_task_orient(pgabb_blocks_t b, uint32_t* dir, 
  * output may be NULL. */
 PGABB_API pgabb_status_t pgabb_get_pieces(pgabb_blocks_t b, uint32_t* task, uint32_t* row_begin,
                                 uint32_t* row_end, uint64_t* cost, int32_t* owner);
+
+/* Streaming residency (S9, "overlapping the next copy with the
+ * computation"): the per-wave timeline of the last count made with PGABB_COUNT_TRACE,
+ * four doubles per wave -- copy start, copy end (copy stream), compute start, compute
+ * end (count stream) -- in ms from the start of the call.  *nwaves receives the wave
+ * count; trace (HOST double[4 * nwaves]) may be NULL to query it.  Synchronous.
+ * Errors: EINVAL (NULL handle or nwaves, no traced streaming count yet), ECUDA. */
+PGABB_API pgabb_status_t pgabb_get_wave_trace(pgabb_blocks_t b, double* trace, uint64_t* nwaves);
 
 /* Frees device and pinned-host memory.  NULL is a no-op. */
 PGABB_API void pgabb_free(pgabb_blocks_t b);

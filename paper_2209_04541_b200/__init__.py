@@ -103,10 +103,12 @@ class Blocks:
         self.free()
 
     # --- S9..S11 ---
-    def triangle_count(self, stream=None, d_count=None, task_counts: bool = False, sync: bool = True):
+    def triangle_count(self, stream=None, d_count=None, task_counts: bool = False, sync: bool = True,
+                       trace: bool = False):
         """This rank's triangle count (host int).  stream: a cudaStream_t int or torch
         stream; d_count: device pointer (int) receiving the count; task_counts: also
-        return the per-task counts."""
+        return the per-task counts; trace: record the streaming waves' timeline
+        (read with wave_trace())."""
         o = _abi.CountOpts()
         if stream is not None:
             o.cuda_stream = _stream_arg(stream)
@@ -117,11 +119,23 @@ class Blocks:
             o.task_counts = tc.ctypes.data_as(_abi.u64p)
         if not sync:
             o.flags = _abi.COUNT_ASYNC
+        if trace:
+            o.flags |= _abi.COUNT_TRACE
         out = ctypes.c_uint64(0)
         _ck(_lib.pgabb_triangle_count(self._h, ctypes.byref(o), ctypes.byref(out)), "pgabb_triangle_count")
         if not sync:
             return None
         return (int(out.value), tc[:self.ntasks]) if task_counts else int(out.value)
+
+    def wave_trace(self):
+        """Per-wave timeline of the last traced streaming count: float64[waves, 4] =
+        (copy start, copy end, compute start, compute end), ms from the call start."""
+        nw = ctypes.c_uint64(0)
+        _ck(_lib.pgabb_get_wave_trace(self._h, None, ctypes.byref(nw)), "pgabb_get_wave_trace")
+        out = np.zeros(max(4 * nw.value, 1), np.float64)
+        _ck(_lib.pgabb_get_wave_trace(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                      ctypes.byref(nw)), "pgabb_get_wave_trace")
+        return out[:4 * nw.value].reshape(-1, 4)
 
     # --- per-vertex counts (SURVEY §8(f) NEXT-1) ---
     def vertex_triangles(self, stream=None, out=None, sync: bool = True, roles: str = "all",
@@ -312,13 +326,18 @@ def vertex_triangles_two_pass(n: int, src, dst, p: int = 0, **kw):
     middle vertex of every triangle from the forward handle (row totals and pair
     counts: no per-hit atomics), the highest vertex as the LOWEST of the handle
     built on the reversed degree order.  Returns (tv, T)."""
+    import torch
+    dev = kw.get("device", -1)
+    out = torch.zeros(max(n, 1), dtype=torch.int64,
+                      device=torch.device("cuda", dev) if dev is not None and dev >= 0 else "cuda")
     with build_blocks(n, src, dst, p=p, **kw) as f:
-        t1, T = f.vertex_triangles(roles="low+mid")
+        _, T = f.vertex_triangles(out=out, roles="low+mid")
     with build_blocks(n, src, dst, p=p, reverse_order=True, **kw) as r:
-        t2, T2 = r.vertex_triangles(roles="low")
+        # the second pass adds into the first on the device (PGABB_OUT_ACCUMULATE)
+        _, T2 = r.vertex_triangles(out=out, roles="low", accumulate=True)
     if T2 != T:
         raise RuntimeError(f"forward and reversed counts differ: {T} != {T2}")
-    return t1 + t2, T
+    return out[:n].cpu().numpy().astype(np.uint64), T
 
 
 def triangle_count(n: int, src, dst, **kw) -> int:

@@ -27,6 +27,7 @@ COUNT_ASYNC = 1
 OUT_DEVICE = 2
 ROLE_LOW, ROLE_MID, ROLE_HIGH = 4, 8, 16
 OUT_ACCUMULATE = 32
+COUNT_TRACE = 64
 
 
 class BuildOpts(ctypes.Structure):
@@ -72,6 +73,7 @@ SIGNATURES = [
     ("pgabb_get_tasks", ctypes.c_int, [vp, u32p, u64p, u64p]),
     ("pgabb_get_task_orient", ctypes.c_int, [vp, u32p, u64p, u64p]),
     ("pgabb_get_pieces", ctypes.c_int, [vp, u32p, u32p, u32p, u64p, i32p]),
+    ("pgabb_get_wave_trace", ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), u64p]),
     ("pgabb_free", None, [vp]),
     ("pgabb_last_error", ctypes.c_char_p, []),
     ("pgabb_version", ctypes.c_char_p, []),

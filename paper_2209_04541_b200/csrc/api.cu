@@ -65,7 +65,6 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     h_col.release();
     h_rowptr.release();
     h_bitmap.release();
-    d_wave_pieces.release();
     d_wave_tasks.release();
     d_arena[0].release();
     d_arena[1].release();
@@ -81,6 +80,7 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     h_result.release();
     for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_mid, ev_last})
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : trace_ev) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (prev >= 0) cudaSetDevice(prev);
 }
@@ -108,7 +108,8 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
     pgabb_status_t st = guarded([&] {
         if (!out) fail(PGABB_EINVAL, "out is NULL");
         if (m > 0 && (!src || !dst)) fail(PGABB_EINVAL, "src/dst NULL with m > 0");
-        if (n >= (1u << 31)) fail(PGABB_ERANGE, "n >= 2^31 is not supported");
+        // n < 2^32 (uint32 ids) and |E| are unbounded here; a block holding >= 2^32
+        // edges is ERANGE (its offsets are 32-bit), checked by the build
         pgabb_build_opts_t o;
         pgabb_default_build_opts(&o);
         if (opts_in) o = *opts_in;
@@ -147,9 +148,19 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
         if (o.task_weights) h->task_weights.assign(o.task_weights, o.task_weights + o.n_task_weights);
         else if (o.n_task_weights) fail(PGABB_EINVAL, "n_task_weights > 0 with task_weights NULL");
-        build_graph(h, m, src, dst, o.inputs_on_device != 0);
-        plan_pieces(h);
-        upload_work(h);
+        PG_NVTX("pgabb_build_blocks");
+        {
+            PG_NVTX("S1-S7 build_graph");
+            build_graph(h, m, src, dst, o.inputs_on_device != 0);
+        }
+        {
+            PG_NVTX("S8 plan_pieces");
+            plan_pieces(h);
+        }
+        {
+            PG_NVTX("S8/S9 upload_work");
+            upload_work(h);
+        }
         if (h->streaming) {
             plan_waves(h);
             PG_CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
@@ -276,7 +287,9 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->cost_local = b->cost_local;
         s->alg_bytes_total = b->alg_total;
         s->alg_bytes_local = b->alg_local;
-        s->block_bytes = b->d_col.bytes() + b->d_rowptr.bytes() + b->d_bitmap.bytes();
+        // streaming handles keep the pools in pinned host DRAM only
+        s->block_bytes = b->streaming ? 4 * (b->h_col.n + b->h_rowptr.n + b->h_bitmap.n)
+                                      : b->d_col.bytes() + b->d_rowptr.bytes() + b->d_bitmap.bytes();
         s->h2d_bytes_last = b->h2d_last;
         s->launches_last = b->launches_last;
         s->waves = b->waves.size();
@@ -365,6 +378,14 @@ pgabb_status_t pgabb_get_pieces(pgabb_blocks_t b, uint32_t* task, uint32_t* r0, 
             if (cost) cost[k] = P.cost;
             if (owner) owner[k] = P.owner;
         }
+    });
+}
+
+pgabb_status_t pgabb_get_wave_trace(pgabb_blocks_t b, double* trace, uint64_t* nwaves) {
+    return guarded([&] {
+        if (!b || !nwaves) fail(PGABB_EINVAL, "NULL argument");
+        DeviceGuard g(b->device);
+        wave_trace(b, trace, nwaves);
     });
 }
 

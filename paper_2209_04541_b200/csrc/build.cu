@@ -46,6 +46,7 @@ inline int bits_for(uint64_t x) {
     return b;
 }
 
+constexpr uint64_t kUploadChunk = 1ull << 27;   // host tuples per staging chunk (1 GiB of u32 pairs)
 constexpr uint64_t kMidSaving = 2;   // R25 auto: saved streamed ids per visit needed for MID
 
 struct CutsArg {
@@ -275,60 +276,37 @@ __global__ void k_task_costs(CostArg a, int i, int j) {
     }
 }
 
-// ---- S5c transposes (DESIGN R25, MID orientation) ---------------------------
-// key = block id << 32 | local col v, value = the edge's position k in the
-// block-major col pool; a stable sort by key orders each block's entries by
-// (v, u) (u ascending within a column, as the pool is (u, v)-sorted per block).
-__global__ void k_tkeys(const uint64_t* dag, uint64_t mE, int B, CutsArg cu, const uint32_t* col, uint64_t* key,
-                        uint32_t* val) {
-    const uint64_t mask = (1ull << B) - 1;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mE;
+// ---- S5c transposes (DESIGN R25, MID orientation), one block at a time -------
+// key = local col v, value = block-local position e of the edge.
+__global__ void k_tkeys(const uint32_t* col, uint64_t nnz, uint32_t* key, uint32_t* val) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t d = dag[k];
-        const uint32_t b = (uint32_t)(part_of(cu, (uint32_t)(d >> B)) * cu.p + part_of(cu, (uint32_t)(d & mask)));
-        key[k] = ((uint64_t)b << 32) | col[k];
+        key[k] = col[k];
         val[k] = (uint32_t)k;
     }
 }
 
-// tcol[pos] = u (local row of part i), tpos[pos] = k - col_off (block-local position
-// of (u,v) in col).  The sorted entries of block b occupy the block's own range.
-__global__ void k_tfill(const uint64_t* dag, uint64_t mE, int B, CutsArg cu, const uint64_t* key,
-                        const uint32_t* val, const unsigned long long* off, uint32_t* tcol, uint32_t* tpos) {
-    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < mE;
+// after the stable sort by v: tpos[q] = e, tcol[q] = the local row u of edge e.
+__global__ void k_tfill(const uint64_t* dag, uint64_t nnz, int B, uint32_t row_base, const uint32_t* val,
+                        uint32_t* tcol, uint32_t* tpos) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nnz;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = val[q];
-        const uint32_t b = (uint32_t)(key[q] >> 32);
-        const uint32_t i = b / (uint32_t)cu.p;
-        tcol[q] = (uint32_t)(dag[k] >> B) - cu.c[i];
-        tpos[q] = (uint32_t)(k - off[b]);
+        const uint32_t e = val[q];
+        tcol[q] = (uint32_t)(dag[e] >> B) - row_base;
+        tpos[q] = e;
     }
 }
 
-// transposed rowptr of the present blocks: entry t of block b (ncols + 1 entries)
-// = number of b's entries with local col < t (lower bound over the sorted keys).
-struct TBlockDev {
-    unsigned long long off, nnz, trp_off;
-    uint32_t ncols, bid;
-};
-__global__ void k_trowptr(const uint64_t* key, const TBlockDev* blk, const unsigned long long* start, int nblk,
-                          unsigned long long total, uint32_t* rowptr) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+// transposed rowptr: trp[t] = number of entries with local col < t, t = 0..ncols.
+__global__ void k_trowptr(const uint32_t* key, uint64_t nnz, uint32_t ncols, uint32_t* trp) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ncols;
          t += (uint64_t)gridDim.x * blockDim.x) {
-        int lo = 0, hi = nblk;   // last block with start <= t
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (start[mid] <= t) lo = mid; else hi = mid;
-        }
-        const TBlockDev bd = blk[lo];
-        const uint64_t target = ((uint64_t)bd.bid << 32) | (uint64_t)(t - start[lo]);
-        uint64_t a = 0, z = bd.nnz;
-        const uint64_t* kk = key + bd.off;
+        uint64_t a = 0, z = nnz;
         while (a < z) {
             const uint64_t mid = a + ((z - a) >> 1);
-            if (kk[mid] < target) a = mid + 1; else z = mid;
+            if (key[mid] < t) a = mid + 1; else z = mid;
         }
-        rowptr[bd.trp_off + (t - start[lo])] = (uint32_t)a;
+        trp[t] = (uint32_t)a;
     }
 }
 
@@ -578,43 +556,57 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         return;
     }
 
-    // ---- upload + validate --------------------------------------------------
-    DBuf<uint32_t> d_s, d_d;
-    const uint32_t *s = src, *d = dst;
+    // ---- upload + validate + S1 canonicalise ----------------------------------
+    // Host tuples go up in chunks through a staging buffer and become keys on the
+    // way, so the build never holds the raw tuples and both key buffers at once.
     // device tuples may still be in flight on the caller's streams (a producer
     // kernel, a copy): the build reads them on the handle's non-blocking stream,
     // which no caller stream orders against, so wait for all device work first
     if (on_device) PG_CK(cudaDeviceSynchronize());
-    if (!on_device) {
-        d_s.alloc(m);
-        d_d.alloc(m);
-        PG_CK(cudaMemcpyAsync(d_s.p, src, m * 4, cudaMemcpyHostToDevice, st));
-        PG_CK(cudaMemcpyAsync(d_d.p, dst, m * 4, cudaMemcpyHostToDevice, st));
-        s = d_s.p;
-        d = d_d.p;
-    }
-    DBuf<int> d_bad;
-    d_bad.alloc(1);
-    PG_CK(cudaMemsetAsync(d_bad.p, 0, 4, st));
-    k_check_ids<<<grid_for(m), kThreads, 0, st>>>(s, d, m, n, d_bad.p);
-    PG_LAUNCH_CHECK();
-    int bad = 0;
-    PG_CK(cudaMemcpyAsync(&bad, d_bad.p, 4, cudaMemcpyDeviceToHost, st));
-    PG_CK(cudaStreamSynchronize(st));
-    if (bad) fail(PGABB_EINVAL, "vertex id >= n in the input tuples");
-
-    // ---- S1 canonicalise ----------------------------------------------------
     DBuf<uint64_t> keys, keys2;
     keys.alloc(m);
+    {
+        DBuf<int> d_bad;
+        d_bad.alloc(1);
+        PG_CK(cudaMemsetAsync(d_bad.p, 0, 4, st));
+        const uint64_t chunk = on_device ? m : std::min<uint64_t>(m, kUploadChunk);
+        DBuf<uint32_t> d_s, d_d;
+        if (!on_device) {
+            d_s.alloc(chunk);
+            d_d.alloc(chunk);
+        }
+        for (uint64_t c0 = 0; c0 < m; c0 += chunk) {
+            const uint64_t cn = std::min(chunk, m - c0);
+            const uint32_t *s = src + c0, *d = dst + c0;
+            if (!on_device) {
+                PG_CK(cudaMemcpyAsync(d_s.p, s, cn * 4, cudaMemcpyHostToDevice, st));
+                PG_CK(cudaMemcpyAsync(d_d.p, d, cn * 4, cudaMemcpyHostToDevice, st));
+                s = d_s.p;
+                d = d_d.p;
+            }
+            k_check_ids<<<grid_for(cn), kThreads, 0, st>>>(s, d, cn, n, d_bad.p);
+            PG_LAUNCH_CHECK();
+            k_make_keys<<<grid_for(cn), kThreads, 0, st>>>(s, d, cn, B, sent, keys.p + c0);
+            PG_LAUNCH_CHECK();
+            if (!on_device) PG_CK(cudaStreamSynchronize(st));   // the staging buffer is reused
+        }
+        int bad = 0;
+        PG_CK(cudaMemcpyAsync(&bad, d_bad.p, 4, cudaMemcpyDeviceToHost, st));
+        PG_CK(cudaStreamSynchronize(st));
+        if (bad) fail(PGABB_EINVAL, "vertex id >= n in the input tuples");
+    }
     keys2.alloc(m);
-    k_make_keys<<<grid_for(m), kThreads, 0, st>>>(s, d, m, B, sent, keys.p);
-    PG_LAUNCH_CHECK();
-    d_s.release();
-    d_d.release();
     const int kbits = std::min(64, 2 * B);
-    cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, (int64_t)m, 0, kbits, st);
-    }, st, tmp);
+    {   // DoubleBuffer sort: O(P) temporary storage instead of another m keys
+        cub::DoubleBuffer<uint64_t> db(keys.p, keys2.p);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, db, (int64_t)m, 0, kbits, st);
+        }, st, tmp);
+        if (db.Current() != keys2.p) {   // sorted keys in keys2
+            std::swap(keys.p, keys2.p);
+            std::swap(keys.n, keys2.n);
+        }
+    }
     DBuf<unsigned long long> d_cnt;
     d_cnt.alloc(2);
     cub_call([&](void* t, size_t& b) {
@@ -629,7 +621,8 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_COPY_SYNC(&last, keys.p + (mE - 1), 8, st);
         if (last == sent) --mE;
     }
-    if (mE >= (1ull << 32)) fail(PGABB_ERANGE, "|E| >= 2^32 is not supported");
+    // |E| is 64-bit throughout (pool offsets, work lists); only a single block's
+    // edges are indexed in 32 bits (checked in S5)
     h->m_edges = mE;
     keys2.release();
 
@@ -665,9 +658,14 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
     if (mE) {
         k_orient<<<grid_for(mE), kThreads, 0, st>>>(keys.p, mE, B, h->d_rank.p);
         PG_LAUNCH_CHECK();
+        cub::DoubleBuffer<uint64_t> db(keys.p, keys2.p);
         cub_call([&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortKeys(t, b, keys.p, keys2.p, (int64_t)mE, 0, kbits, st);
+            return cub::DeviceRadixSort::SortKeys(t, b, db, (int64_t)mE, 0, kbits, st);
         }, st, tmp);
+        if (db.Current() != keys2.p) {
+            std::swap(keys.p, keys2.p);
+            std::swap(keys.n, keys2.n);
+        }
     }
     keys.release();
     uint64_t* dag = keys2.p;   // DAG edges sorted by (row, col) in rank space
@@ -721,9 +719,17 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         k_block_ids<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, bid.p);
         PG_LAUNCH_CHECK();
         const int bbits = std::max(1, bits_for(nb - 1));
-        cub_call([&](void* t, size_t& b) {   // stable: (row, col) order kept inside a block
-            return cub::DeviceRadixSort::SortPairs(t, b, bid.p, bid2.p, dag, dag2.p, (int64_t)mE, 0, bbits, st);
-        }, st, tmp);
+        {   // stable: (row, col) order kept inside a block; DoubleBuffer: O(P) temporary
+            cub::DoubleBuffer<uint32_t> dbk(bid.p, bid2.p);
+            cub::DoubleBuffer<uint64_t> dbv(dag, dag2.p);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortPairs(t, b, dbk, dbv, (int64_t)mE, 0, bbits, st);
+            }, st, tmp);
+            if (dbk.Current() != bid2.p) std::swap(bid.p, bid2.p);   // same sizes
+            if (dbv.Current() != dag2.p) {   // sorted pairs landed in dag: keep dag2 the result
+                PG_CK(cudaMemcpyAsync(dag2.p, dag, mE * 8, cudaMemcpyDeviceToDevice, st));
+            }
+        }
         bid.release();
         DBuf<unsigned long long> d_off;
         d_off.alloc(nb + 1);
@@ -746,6 +752,10 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
         PG_CK(cudaMemcpyAsync(dag, dag2.p, mE * 8, cudaMemcpyDeviceToDevice, st));
         PG_CK(cudaStreamSynchronize(st));
     }
+    for (uint32_t b = 0; b < nb; ++b)
+        if (off[b + 1] - off[b] >= (1ull << 32))
+            fail(PGABB_ERANGE, "block (" + std::to_string(b / p) + "," + std::to_string(b % p) +
+                                   ") holds >= 2^32 edges (block-local offsets are 32-bit): use a larger p");
     h->blocks.assign(nb, BlockInfo{});
     uint64_t rp_total = 0;
     std::vector<BlockDev> bdev(nb);
@@ -768,16 +778,12 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
             if (b.present) present.push_back(bdev[i * p + j]);
         }
     const uint64_t rp_plain = rp_total;
-    std::vector<TBlockDev> tpresent;
-    std::vector<unsigned long long> trp_start;
     if (h->has_t)
         for (uint32_t i = 0; i < p; ++i)
             for (uint32_t j = i; j < p; ++j) {
                 BlockInfo& b = h->blocks[i * p + j];
                 if (!b.present) continue;
                 b.trp_off = rp_total;
-                trp_start.push_back(rp_total - rp_plain);
-                tpresent.push_back(TBlockDev{b.col_off, b.nnz, b.trp_off, b.ncols, i * p + j});
                 rp_total += (uint64_t)b.ncols + 1;
             }
     h->d_rowptr.alloc(std::max<uint64_t>(rp_total, 1));
@@ -796,39 +802,37 @@ void build_graph(pgabb_blocks_s* h, uint64_t m, const uint32_t* src, const uint3
     }
 
     // ---- S5c transposes of the blocks (MID orientation, DESIGN R25) ----------
+    // Per block: a stable sort of (local col v, position e) -- u order is kept
+    // within a column as the block is (u, v)-sorted -- gives tpos; tcol = the row
+    // of each position; the transposed rowptr is a lower bound over the sorted v.
+    // One block at a time, so the temporary memory is that of the largest block.
     if (h->has_t && mE) {
-        DBuf<uint64_t> tk, tk2;
-        DBuf<uint32_t> tv, tv2;
-        tk.alloc(mE);
-        tv.alloc(mE);
-        k_tkeys<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, h->d_col.p, tk.p, tv.p);
-        PG_LAUNCH_CHECK();
-        tk2.alloc(mE);
-        tv2.alloc(mE);
-        const int bbits = std::max(1, bits_for(nb - 1));
-        cub_call([&](void* t, size_t& b) {   // stable: u order kept within a column
-            return cub::DeviceRadixSort::SortPairs(t, b, tk.p, tk2.p, tv.p, tv2.p, (int64_t)mE, 0, 32 + bbits, st);
-        }, st, tmp);
-        tk.release();
-        tv.release();
-        DBuf<unsigned long long> d_off;
-        d_off.alloc(nb + 1);
-        PG_CK(cudaMemcpyAsync(d_off.p, off.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
-        k_tfill<<<grid_for(mE), kThreads, 0, st>>>(dag, mE, B, cu, tk2.p, tv2.p, d_off.p, h->d_col.p + h->tcol_base,
-                                                    h->d_col.p + h->tpos_base);
-        PG_LAUNCH_CHECK();
-        const uint64_t ttotal = rp_total - rp_plain;
-        DBuf<TBlockDev> d_tb;
-        DBuf<unsigned long long> d_ts;
-        d_tb.alloc(tpresent.size());
-        d_ts.alloc(trp_start.size());
-        PG_CK(cudaMemcpyAsync(d_tb.p, tpresent.data(), tpresent.size() * sizeof(TBlockDev), cudaMemcpyHostToDevice,
-                              st));
-        PG_CK(cudaMemcpyAsync(d_ts.p, trp_start.data(), trp_start.size() * 8, cudaMemcpyHostToDevice, st));
-        // entry t of the flattened transposed rowptrs -> block by start, then lower bound
-        k_trowptr<<<grid_for(ttotal), kThreads, 0, st>>>(tk2.p, d_tb.p, d_ts.p, (int)tpresent.size(), ttotal,
-                                                         h->d_rowptr.p);
-        PG_LAUNCH_CHECK();
+        uint64_t maxnnz = 0;
+        for (const BlockInfo& b : h->blocks) maxnnz = std::max(maxnnz, b.nnz);
+        DBuf<uint32_t> kv, kv2, iv, iv2;
+        kv.alloc(maxnnz);
+        kv2.alloc(maxnnz);
+        iv.alloc(maxnnz);
+        iv2.alloc(maxnnz);
+        for (uint32_t i = 0; i < p; ++i)
+            for (uint32_t j = i; j < p; ++j) {
+                const BlockInfo& b = h->blocks[i * p + j];
+                if (!b.present) continue;
+                k_tkeys<<<grid_for(b.nnz), kThreads, 0, st>>>(h->d_col.p + b.col_off, b.nnz, kv.p, iv.p);
+                PG_LAUNCH_CHECK();
+                const int cb = std::max(1, bits_for(b.ncols));
+                cub::DoubleBuffer<uint32_t> dbk(kv.p, kv2.p), dbv(iv.p, iv2.p);
+                cub_call([&](void* t, size_t& bt) {
+                    return cub::DeviceRadixSort::SortPairs(t, bt, dbk, dbv, (int64_t)b.nnz, 0, cb, st);
+                }, st, tmp);
+                k_tfill<<<grid_for(b.nnz), kThreads, 0, st>>>(dag + b.col_off, b.nnz, B, h->cuts[i], dbv.Current(),
+                                                               h->d_col.p + h->tcol_base + b.col_off,
+                                                               h->d_col.p + h->tpos_base + b.col_off);
+                PG_LAUNCH_CHECK();
+                k_trowptr<<<grid_for((uint64_t)b.ncols + 1), kThreads, 0, st>>>(dbk.Current(), b.nnz, b.ncols,
+                                                                               h->d_rowptr.p + b.trp_off);
+                PG_LAUNCH_CHECK();
+            }
         PG_CK(cudaStreamSynchronize(st));
     }
 
@@ -1144,7 +1148,7 @@ void plan_waves(pgabb_blocks_s* h) {
     const uint64_t half = h->budget / 2 / 4;   // words per arena
     const size_t nt = h->tasks.size();
     h->waves.clear();
-    std::vector<WavePiece> wpieces;
+    size_t npieces = 0;                 // owned pieces placed so far (locality order)
     std::vector<TaskDev> wtasks;
     const std::vector<size_t> order = locality_order(h);
     // (block, part) -> arena word offset of the current wave
@@ -1157,14 +1161,18 @@ void plan_waves(pgabb_blocks_s* h) {
     std::vector<TaskDev> cur_tasks;
     auto open_wave = [&]() {
         cur = Wave{};
-        cur.piece_begin = wpieces.size();
+        cur.piece_begin = npieces;
         prev_placed.swap(placed);
         placed.clear();
         cur_tasks.assign(nt, TaskDev{});
     };
     auto close_wave = [&]() {
-        if (cur.rows == 0) return;
-        cur.piece_end = wpieces.size();
+        if (npieces == cur.piece_begin) return;
+        cur.piece_end = npieces;
+        cur.item_begin = h->piece_item_off[cur.piece_begin];
+        cur.item_end = h->piece_item_off[cur.piece_end];
+        cur.light_begin = h->piece_light_off[cur.piece_begin];
+        cur.light_end = h->piece_light_off[cur.piece_end];
         cur.task_table = h->waves.size();
         wtasks.insert(wtasks.end(), cur_tasks.begin(), cur_tasks.end());
         h->waves.push_back(cur);
@@ -1202,13 +1210,9 @@ void plan_waves(pgabb_blocks_s* h) {
             cur.words += wd;
         }
         cur_tasks[w.task] = make_taskdev(h, T, [&](PartRef r) { return placed[{r.block, r.part}]; });
-        wpieces.push_back(WavePiece{cur.rows, w.task, w.r0});
-        cur.rows += w.r1 - w.r0;
+        ++npieces;
     }
     close_wave();
-    h->d_wave_pieces.alloc(std::max<size_t>(wpieces.size(), 1));
-    if (!wpieces.empty())
-        PG_COPY_SYNC(h->d_wave_pieces.p, wpieces.data(), wpieces.size() * sizeof(WavePiece), h->stream);
     h->d_wave_tasks.alloc(std::max<size_t>(wtasks.size(), 1));
     if (!wtasks.empty())
         PG_COPY_SYNC(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), h->stream);
@@ -1312,8 +1316,6 @@ void upload_work(pgabb_blocks_s* h) {
         for (int q = 0; q < np; ++q) words += part_words(h, parts[q]);
         h->max_task_bytes = std::max(h->max_task_bytes, 4 * words);
     }
-    if (h->streaming) return;   // streaming residency enumerates rows implicitly per wave
-
     // Row items of the owned pieces, laid out for L2 locality: pieces in task
     // order (x desc, j desc, i asc) so that the warps running concurrently share
     // the blocks of one task (and the hub column part is done first), rows
@@ -1344,7 +1346,10 @@ void upload_work(pgabb_blocks_s* h) {
             return cub::DeviceScan::ExclusiveSum(tp, b, lf.p, lpos.p, (int64_t)nr + 1, st);
         }, st, tmp);
     };
-    // pass 1: count per piece
+    // pass 1: count per piece; item offsets per piece in locality order (the waves of
+    // streaming residency are contiguous ranges of them)
+    h->piece_item_off.assign(order.size() + 1, 0);
+    h->piece_light_off.assign(order.size() + 1, 0);
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
@@ -1357,9 +1362,11 @@ void upload_work(pgabb_blocks_s* h) {
         piece_light[k] = cnt[1];
     }
     uint64_t nitems = 0, nlight = 0;
-    for (size_t k = 0; k < piece_items.size(); ++k) {
-        nitems += piece_items[k];
-        nlight += piece_light[k];
+    for (size_t q = 0; q < order.size(); ++q) {
+        nitems += piece_items[order[q]];
+        nlight += piece_light[order[q]];
+        h->piece_item_off[q + 1] = nitems;
+        h->piece_light_off[q + 1] = nlight;
     }
     h->n_items = nitems;
     h->n_light = nlight;

@@ -34,7 +34,7 @@ struct CcBlock {               // one non-empty block of the grid
 };
 
 __global__ void k_cc_init(uint32_t* C, uint32_t n) {
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) C[x] = x;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x) C[x] = x;
 }
 
 // HOOK over every edge of every block: a warp claims 32 consecutive global rows,
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k_cc_hook(const CcBlock* __restrict__ blk
 // and is seen by the other threads walking through x, so deep hook trees (grids,
 // chains) collapse in O(log depth) steps instead of one step per level.
 __global__ void k_cc_link(uint32_t* C, uint32_t n) {
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t c = C[x], cc;
         while (c != (cc = C[c])) {
             c = cc;
@@ -128,11 +128,11 @@ __global__ void k_cc_minorig(const uint32_t* __restrict__ rank, const uint32_t* 
                              uint32_t* M) {
     // a giant component sends every v to one address: lanes with the same root
     // reduce first, and a proposal that cannot lower the current minimum is dropped
-    const uint32_t n32 = (n + 31) & ~31u;   // whole warps take part in the warp reductions
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n32; v += gridDim.x * blockDim.x) {
+    const uint64_t n32 = ((uint64_t)n + 31) & ~31ull;   // whole warps take part in the warp reductions
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n32; v += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t root = v < n ? C[rank[v]] : 0xffffffffu;
         const uint32_t same = __match_any_sync(0xffffffffu, root);
-        const uint32_t m = __reduce_min_sync(same, v);
+        const uint32_t m = __reduce_min_sync(same, (uint32_t)v);
         if (v < n && v == m && m < *(volatile uint32_t*)&M[root]) atomicMin(&M[root], m);
     }
 }
@@ -141,7 +141,7 @@ __global__ void k_cc_labels(const uint32_t* __restrict__ rank, const uint32_t* _
                             const uint32_t* __restrict__ M, uint32_t n, uint32_t* labels,
                             unsigned long long* ncomp) {
     uint32_t roots = 0;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t l = M[C[rank[v]]];
         labels[v] = l;
         roots += (l == v);

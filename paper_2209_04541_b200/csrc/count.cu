@@ -525,59 +525,9 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
     return acc;
 }
 
-// Streaming residency: a warp claims the next 32 rows of the wave, one per lane;
-// each lane decodes its row (piece by binary search over the wave's piece table),
-// reads |A_ix[u]| and |A_ij[u]| and drops empty rows and light rows (k_row_flags's
-// predicate; those are k_tc_light<IMPLICIT>'s).  Returns the ballot of the heavy
-// rows (0 only when the wave is exhausted) with each lane's (task, row).
-__device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next, unsigned long long nitems,
-                                                        const WavePiece* __restrict__ wp, int nwp,
-                                                        const TaskDev* __restrict__ tasks,
-                                                        const uint32_t* __restrict__ col,
-                                                        const uint32_t* __restrict__ rowptr, int lane,
-                                                        uint32_t& t_l, uint32_t& u_l) {
-    for (;;) {
-        unsigned long long b = 0;
-        if (lane == 0) b = atomicAdd(next, 32ull);
-        b = __shfl_sync(0xffffffffu, b, 0);
-        if (b >= nitems) return 0u;
-        const unsigned long long idx = b + lane;
-        bool heavy = false;
-        if (idx < nitems) {
-            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
-            }
-            t_l = wp[lo].task;
-            u_l = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
-            const TaskDev& T = tasks[t_l];
-            const uint32_t la = __ldg(rowptr + T.s_rp + u_l + 1) - __ldg(rowptr + T.s_rp + u_l);
-            const uint32_t e0 = __ldg(rowptr + T.n_rp + u_l), e1 = __ldg(rowptr + T.n_rp + u_l + 1);
-            heavy = la > 0 && e1 > e0;
-            if (heavy && la <= kLightLa && e1 - e0 <= kLightLe) {
-                bool light = T.t_bm != ~0ull;
-                if (!light) {
-                    uint32_t work = 0;
-                    for (uint32_t e = e0; e < e1; ++e) {
-                        const uint32_t v = __ldg(col + T.n_col + e);
-                        const uint32_t b0 = T.n_pos != ~0ull ? __ldg(col + T.n_pos + e) + 1 : __ldg(rowptr + T.t_rp + v);
-                        work += light_pair_loads(la, __ldg(rowptr + T.t_rp + v + 1) - b0);
-                    }
-                    light = work <= kLightWork;
-                }
-                heavy = !light;
-            }
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, heavy);
-        if (m) return m;
-    }
-}
-
-// IMPLICIT = false: items[] holds the compacted row items (device-resident blocks).
-// IMPLICIT = true (streaming residency): item idx is row idx of the wave's piece
-// table wp[0..nwp) (empty and light rows are dropped by implicit_heavy_rows), and
-// the pool pointers all point at the wave's staging arena.
+// items[] holds the row items in locality order: the whole rank's (device-resident
+// blocks) or one wave's range of them (streaming residency: the task table and the
+// pool pointers then all point at the wave's staging arena).
 // VM > 0 (per-vertex counts, NEXT-1): tv[rank-space id] += the triangles found
 // here that contain the vertex in the requested roles -- u gets the row total
 // (VM >= 1), v each pair's c_uv (VM >= 2), w one per hit (VM >= 3) -- so with
@@ -585,10 +535,9 @@ __device__ __forceinline__ uint32_t implicit_heavy_rows(unsigned long long* next
 // TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
 #define IROW(M, R_, ...) \
     (npos ? intersect_row<M, R_, VM, true>(__VA_ARGS__) : intersect_row<M, R_, VM, false>(__VA_ARGS__))
-template <bool IMPLICIT, int VM, bool TIMED>
+template <int VM, bool TIMED>
 __global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
-k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restrict__ wp, int nwp,
-          unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
+k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
           unsigned long long* __restrict__ next, unsigned long long* __restrict__ cyc) {
@@ -605,10 +554,9 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     __syncwarp();
     // Warps claim kRowChunk items at a time from one counter, so the items in
     // flight stay a narrow window of the locality-ordered list (the A_jx blocks
-    // they share stay in L2).  IMPLICIT: item idx is row idx of the wave.
+    // they share stay in L2).
     unsigned long long claim_end = 0;
-    unsigned long long idx = IMPLICIT ? 0 : claim_items(next, nitems, lane, claim_end);
-    uint32_t hrows = 0, t_l = 0, u_l = 0;            // IMPLICIT: heavy rows of the claimed window
+    unsigned long long idx = claim_items(next, nitems, lane, claim_end);
     uint32_t cur_t = 0;                              // task of the warp's running count
     unsigned long long acc_t = 0;
 #ifdef PGABB_PROF
@@ -617,22 +565,12 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
     unsigned long long pt = clock64();
 #endif
     for (;;) {
-        uint32_t t, u, chunk = 0;
-        if (IMPLICIT) {
-            if (!hrows && !(hrows = implicit_heavy_rows(next, nitems, wp, nwp, tasks, col, rowptr, lane, t_l, u_l)))
-                break;
-            const int bl = __ffs(hrows) - 1;
-            hrows &= hrows - 1;
-            t = __shfl_sync(0xffffffffu, t_l, bl);
-            u = __shfl_sync(0xffffffffu, u_l, bl);
-        } else {
-            if (idx >= nitems) break;
-            const unsigned long long it = __ldg(items + idx);
-            t = (uint32_t)(it >> 48);
-            chunk = (uint32_t)(it >> 32) & 0xffffu;
-            u = (uint32_t)it;
-            idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
-        }
+        if (idx >= nitems) break;
+        const unsigned long long it = __ldg(items + idx);
+        const uint32_t t = (uint32_t)(it >> 48);
+        const uint32_t chunk = (uint32_t)(it >> 32) & 0xffffu;
+        const uint32_t u = (uint32_t)it;
+        idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
         const long long c0 = TIMED ? clock64() : 0;
         // kernel roles (internal.h TaskDev, DESIGN R25): u is the item's row vertex,
         // A its held list, vcol its neighbours (chunk `chunk` of them), Bc/rp_jx the
@@ -640,10 +578,8 @@ k_tc_rows(const unsigned long long* __restrict__ items, const WavePiece* __restr
         const TaskDev T = tasks[t];
         const uint32_t a0 = __ldg(rowptr + T.s_rp + u), a1 = __ldg(rowptr + T.s_rp + u + 1);
         uint32_t e0 = __ldg(rowptr + T.n_rp + u), e1 = __ldg(rowptr + T.n_rp + u + 1);
-        if (!IMPLICIT) {
-            e0 += chunk * kChunkNbrs;
-            e1 = min(e1, e0 + kChunkNbrs);
-        }
+        e0 += chunk * kChunkNbrs;
+        e1 = min(e1, e0 + kChunkNbrs);
         const uint32_t la = a1 - a0;
         const uint32_t* __restrict__ A = col + T.s_col + a0;
         const uint32_t* __restrict__ Bc = col + T.t_col;
@@ -907,12 +843,11 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
     return acc;
 }
 
-// IMPLICIT (streaming residency): item idx is row idx of the wave's piece table
-// wp[0..nwp); the thread reads the row's offsets itself and takes the row only if
-// it is light by k_row_flags's predicate (the heavy kernel skips exactly those).
-template <int VM, bool TIMED, bool IMPLICIT>
+// items: the whole rank's light items, or one wave's range of them (streaming: the
+// task table and pools then point at the wave's arena).
+template <int VM, bool TIMED>
 __global__ void __launch_bounds__(kLightThreads, PGABB_LIGHT_MINB)
-k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, int nwp, unsigned long long nitems,
+k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
            unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
@@ -926,49 +861,23 @@ k_tc_light(const uint4* __restrict__ items, const WavePiece* __restrict__ wp, in
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= nitems) break;
     uint4 it_next = make_uint4(0, 0, 0, 0);   // PGABB_LIGHT_PREFETCH: the next item, loaded a step early
-    if (!IMPLICIT && kLightPrefetch && base + lane < nitems) it_next = __ldg(items + base + lane);
+    if (kLightPrefetch && base + lane < nitems) it_next = __ldg(items + base + lane);
     for (int r = 0; r < kLightChunk; ++r) {
         const unsigned long long idx = base + 32 * r + lane;
         if (idx >= nitems) break;
-        uint32_t t, u, la, a0, e0, e1;
-        if (IMPLICIT) {
-            int lo = 0, hi = nwp;   // last piece with row_prefix <= idx
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (wp[mid].row_prefix <= idx) lo = mid; else hi = mid;
-            }
-            t = wp[lo].task;
-            u = wp[lo].r0 + (uint32_t)(idx - wp[lo].row_prefix);
-            const TaskDev& Tq = tasks[t];
-            a0 = __ldg(rowptr + Tq.s_rp + u);
-            la = __ldg(rowptr + Tq.s_rp + u + 1) - a0;
-            e0 = __ldg(rowptr + Tq.n_rp + u);
-            e1 = __ldg(rowptr + Tq.n_rp + u + 1);
-            if (la == 0 || e1 == e0 || la > kLightLa || e1 - e0 > kLightLe) continue;
-            if (Tq.t_bm == ~0ull) {
-                uint32_t work = 0;
-                for (uint32_t e = e0; e < e1; ++e) {
-                    const uint32_t v = __ldg(col + Tq.n_col + e);
-                    const uint32_t b0 = Tq.n_pos != ~0ull ? __ldg(col + Tq.n_pos + e) + 1 : __ldg(rowptr + Tq.t_rp + v);
-                    work += light_pair_loads(la, __ldg(rowptr + Tq.t_rp + v + 1) - b0);
-                }
-                if (work > kLightWork) continue;   // a heavy row: the warp kernel's
-            }
+        uint4 it;
+        if (kLightPrefetch) {
+            it = it_next;
+            if (r + 1 < kLightChunk && idx + 32 < nitems) it_next = __ldg(items + idx + 32);
         } else {
-            uint4 it;
-            if (kLightPrefetch) {
-                it = it_next;
-                if (r + 1 < kLightChunk && idx + 32 < nitems) it_next = __ldg(items + idx + 32);
-            } else {
-                it = __ldg(items + idx);
-            }
-            t = it.x & ((1u << kLightTaskBits) - 1);
-            u = it.w;
-            la = (it.x >> kLightTaskBits) & 15u;
-            a0 = it.y;
-            e0 = it.z;
-            e1 = e0 + (it.x >> (kLightTaskBits + 4));
+            it = __ldg(items + idx);
         }
+        const uint32_t t = it.x & ((1u << kLightTaskBits) - 1);
+        const uint32_t u = it.w;
+        const uint32_t la = (it.x >> kLightTaskBits) & 15u;
+        const uint32_t a0 = it.y;
+        const uint32_t e0 = it.z;
+        const uint32_t e1 = e0 + (it.x >> (kLightTaskBits + 4));
         if (t != cur_t) {
             if (acc_t) atomicAdd(&task_counts[cur_t], acc_t);
             if (TIMED && cyc_t) atomicAdd(&cyc[cur_t], cyc_t);
@@ -1051,7 +960,7 @@ __global__ void k_sum_tasks(unsigned long long* tc, int nt, unsigned long long* 
 // accumulate: tv[v] += (PGABB_OUT_ACCUMULATE, the second pass of the two-pass route)
 __global__ void k_gather_tv(const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ tv_rank,
                             uint32_t n, unsigned long long* __restrict__ tv, int accumulate) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
         tv[v] = (accumulate ? tv[v] : 0ull) + tv_rank[rank[v]];
 }
 
@@ -1060,7 +969,7 @@ __global__ void k_gather_tv(const uint32_t* __restrict__ rank, const unsigned lo
 // division is correctly rounded and bit-identical to any other such evaluation.
 __global__ void k_clustering(const uint32_t* __restrict__ deg, const unsigned long long* __restrict__ tv,
                              uint32_t n, double* __restrict__ cc) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t d = deg[v];
         cc[v] = d < 2 ? 0.0 : (2.0 * (double)tv[v]) / (double)(d * (d - 1));
     }
@@ -1151,15 +1060,11 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kRowWarps * 32, sm));
             return sms * std::max(per_sm, 1);
         };
-        grids[0] = setup(k_tc_rows<false, 0, false>, 0);
-        setup(k_tc_rows<true, 0, false>, 0);
-        setup(k_tc_rows<false, 0, true>, 0);
-        grids[1] = setup(k_tc_rows<false, 1, false>, 1);
-        setup(k_tc_rows<true, 1, false>, 1);
-        grids[2] = setup(k_tc_rows<false, 2, false>, 2);
-        setup(k_tc_rows<true, 2, false>, 2);
-        grids[3] = setup(k_tc_rows<false, 3, false>, 3);
-        setup(k_tc_rows<true, 3, false>, 3);
+        grids[0] = setup(k_tc_rows<0, false>, 0);
+        setup(k_tc_rows<0, true>, 0);
+        grids[1] = setup(k_tc_rows<1, false>, 1);
+        grids[2] = setup(k_tc_rows<2, false>, 2);
+        grids[3] = setup(k_tc_rows<3, false>, 3);
         cached_dev = h->device;
     }
     const int grid = grids[vm];
@@ -1172,25 +1077,37 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         if (h->d_tv_rank.n < std::max<uint32_t>(h->n, 1)) h->d_tv_rank.alloc(std::max<uint32_t>(h->n, 1));
         tv = h->d_tv_rank.p;
     }
-    auto rows_kernel = [&](bool implicit) {
-        if (timed) return k_tc_rows<false, 0, true>;
+    auto rows_kernel = [&]() {
+        if (timed) return k_tc_rows<0, true>;
         switch (vm) {
-            case 1: return implicit ? k_tc_rows<true, 1, false> : k_tc_rows<false, 1, false>;
-            case 2: return implicit ? k_tc_rows<true, 2, false> : k_tc_rows<false, 2, false>;
-            case 3: return implicit ? k_tc_rows<true, 3, false> : k_tc_rows<false, 3, false>;
-            default: return implicit ? k_tc_rows<true, 0, false> : k_tc_rows<false, 0, false>;
+            case 1: return k_tc_rows<1, false>;
+            case 2: return k_tc_rows<2, false>;
+            case 3: return k_tc_rows<3, false>;
+            default: return k_tc_rows<0, false>;
         }
     };
-    auto light_kernel = [&](bool implicit) {
-        if (timed) return k_tc_light<0, true, false>;
+    auto light_kernel = [&]() {
+        if (timed) return k_tc_light<0, true>;
         switch (vm) {
-            case 1: return implicit ? k_tc_light<1, false, true> : k_tc_light<1, false, false>;
-            case 2: return implicit ? k_tc_light<2, false, true> : k_tc_light<2, false, false>;
-            case 3: return implicit ? k_tc_light<3, false, true> : k_tc_light<3, false, false>;
-            default: return implicit ? k_tc_light<0, false, true> : k_tc_light<0, false, false>;
+            case 1: return k_tc_light<1, false>;
+            case 2: return k_tc_light<2, false>;
+            case 3: return k_tc_light<3, false>;
+            default: return k_tc_light<0, false>;
         }
+    };
+    static thread_local int light_dev = -1, light_grid = 0;
+    if (light_dev != h->device) {
+        int per_sm = 0;
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false>, kLightThreads, 0));
+        light_grid = sm_count(h->device) * std::max(per_sm, 1);
+        light_dev = h->device;
+    }
+    auto grid_for_light = [&](unsigned long long n) {
+        return (unsigned)std::max<unsigned long long>(
+            1ull, std::min<unsigned long long>(light_grid, (n + kLightThreads - 1) / kLightThreads));
     };
 
+    PG_NVTX(vtx ? "pgabb_vertex_triangles" : "pgabb_triangle_count");
     settle_timing(h);
     begin_call(h, st);
     PG_CK(cudaEventRecord(h->ev0, st));
@@ -1211,8 +1128,8 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         PG_CK(cudaMemsetAsync(h->d_next.p, 0, 2 * sizeof(unsigned long long), st));
         PG_CK(cudaEventRecord(h->ev1, st));
         if (h->n_items) {
-            rows_kernel(false)<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
-                h->d_items.p, nullptr, 0, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
+            rows_kernel()<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
+                h->d_items.p, h->n_items, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
                 h->d_task_counts.p, tv, h->d_next.p + 1, d_cycles);
             PG_LAUNCH_CHECK();
             h->launches_last++;
@@ -1220,20 +1137,9 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         PG_CK(cudaEventRecord(h->ev_mid, st));
         h->light_timed = true;
         if (h->n_light) {
-            static thread_local int light_dev = -1, light_grid = 0;
-            if (light_dev != h->device) {
-                int sms = 0, per_sm = 0;
-                PG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false, false>,
-                                                                    kLightThreads, 0));
-                light_grid = sms * std::max(per_sm, 1);
-                light_dev = h->device;
-            }
-            const unsigned g = (unsigned)std::max<unsigned long long>(
-                1ull, std::min<unsigned long long>(light_grid, (h->n_light + kLightThreads - 1) / kLightThreads));
-            light_kernel(false)<<<g, kLightThreads, 0, st>>>(h->d_light.p, nullptr, 0, h->n_light, h->d_tasks.p, h->d_col.p,
-                                              h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p, tv, h->d_next.p,
-                                              timed ? d_cycles + nt : nullptr);
+            light_kernel()<<<grid_for_light(h->n_light), kLightThreads, 0, st>>>(
+                h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p,
+                tv, h->d_next.p, timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -1246,10 +1152,20 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         PG_CK(cudaEventRecord(h->ev1, st));
         PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev1, 0));
         const uint32_t* pools[3] = {h->h_col.p, h->h_rowptr.p, h->h_bitmap.p};
+        const bool trace = opts && (opts->flags & PGABB_COUNT_TRACE);
+        if (trace) {
+            while (h->trace_ev.size() < 4 * h->waves.size()) {
+                cudaEvent_t e;
+                PG_CK(cudaEventCreate(&e));
+                h->trace_ev.push_back(e);
+            }
+        }
+        h->trace_valid = trace;
         for (size_t k = 0; k < h->waves.size(); ++k) {
             const Wave& wv = h->waves[k];
             const int a = (int)(k & 1);
             if (k >= 2) PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev_done[a], 0));
+            if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k], h->copy_stream));
             for (const StagedBlock& c : wv.copies) {
                 if (c.pool == 3) {   // held by the previous wave: device-to-device from the other arena
                     PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, h->d_arena[1 - a].p + c.src_word,
@@ -1262,26 +1178,32 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
                 h->h2d_last += c.words * 4;
             }
             PG_CK(cudaEventRecord(h->ev_copied[a], h->copy_stream));
+            if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 1], h->copy_stream));
             PG_CK(cudaStreamWaitEvent(st, h->ev_copied[a], 0));
+            if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 2], st));
+            // the wave's ranges of the row items; its task table and all three pool
+            // pointers address the arena
             const uint32_t* base = h->d_arena[a].p;
+            const TaskDev* wt = h->d_wave_tasks.p + wv.task_table * nt;
             PG_CK(cudaMemsetAsync(h->d_next.p + 2, 0, 2 * sizeof(unsigned long long), st));
-            rows_kernel(true)<<<grid_for_items(wv.rows), kRowWarps * 32, smem, st>>>(
-                nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 2,
-                nullptr);
-            PG_LAUNCH_CHECK();
-            h->launches_last++;
-            {
-                const unsigned lg = (unsigned)std::max<unsigned long long>(
-                    1ull, std::min<unsigned long long>((unsigned long long)sm_count(h->device) * 8, (wv.rows + kLightThreads - 1) / kLightThreads));
-                light_kernel(true)<<<lg, kLightThreads, 0, st>>>(
-                    nullptr, h->d_wave_pieces.p + wv.piece_begin, (int)(wv.piece_end - wv.piece_begin), wv.rows,
-                    h->d_wave_tasks.p + wv.task_table * nt, base, base, base, h->d_task_counts.p, tv,
-                    h->d_next.p + 3, nullptr);
+            if (wv.item_end > wv.item_begin) {
+                const unsigned long long ni = wv.item_end - wv.item_begin;
+                rows_kernel()<<<grid_for_items(ni), kRowWarps * 32, smem, st>>>(
+                    h->d_items.p + wv.item_begin, ni, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 2,
+                    nullptr);
+                PG_LAUNCH_CHECK();
+                h->launches_last++;
+            }
+            if (wv.light_end > wv.light_begin) {
+                const unsigned long long nl = wv.light_end - wv.light_begin;
+                light_kernel()<<<grid_for_light(nl), kLightThreads, 0, st>>>(
+                    h->d_light.p + wv.light_begin, nl, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 3,
+                    nullptr);
                 PG_LAUNCH_CHECK();
                 h->launches_last++;
             }
             PG_CK(cudaEventRecord(h->ev_done[a], st));
+            if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 3], st));
         }
     }
     PG_CK(cudaEventRecord(h->ev2, st));
@@ -1310,6 +1232,18 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
     }
     *wrote = true;
     return h->h_result.p[0];
+}
+
+void wave_trace(pgabb_blocks_s* h, double* out, uint64_t* nwaves) {
+    if (!h->trace_valid) fail(PGABB_EINVAL, "no traced streaming count (PGABB_COUNT_TRACE) on this handle");
+    *nwaves = h->waves.size();
+    if (!out) return;
+    PG_CK(cudaEventSynchronize(h->ev3));
+    for (size_t k = 0; k < 4 * h->waves.size(); ++k) {
+        float ms = 0;
+        PG_CK(cudaEventElapsedTime(&ms, h->ev0, h->trace_ev[k]));
+        out[k] = ms;
+    }
 }
 
 void task_times(pgabb_blocks_s* h, uint64_t* ns) {

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pgabb.h"
 
 namespace pgabb {
@@ -22,6 +24,17 @@ struct Error {
 void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 
 #define PG_CK(x) ::pgabb::check_cuda((x), #x, __FILE__, __LINE__)
+
+// NVTX ranges around the build steps and count phases (visible in nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PG_NVTX_CAT2(a, b) a##b
+#define PG_NVTX_CAT(a, b) PG_NVTX_CAT2(a, b)
+#define PG_NVTX(name) ::pgabb::NvtxRange PG_NVTX_CAT(pg_nvtx_, __LINE__)(name)
 #define PG_LAUNCH_CHECK() ::pgabb::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
 // Blocking copy ORDERED ON `st` (cudaMemcpyDefault, UVA).  The handle's stream is
@@ -223,11 +236,6 @@ __host__ __device__ inline uint32_t light_pair_loads(uint32_t la, uint32_t lb) {
 // Streaming residency (S9): host-resident blocks are
 // staged into one of two device arenas per wave of tasks; the copy of wave k+1
 // (copy stream) overlaps the intersections of wave k.
-struct WavePiece {          // one owned piece inside a wave (device table)
-    uint64_t row_prefix;    // first implicit item of the piece within the wave
-    uint32_t task, r0;
-};
-
 struct StagedBlock {        // one H2D copy: pool range -> arena offset (u32 words)
     uint64_t src_word, dst_word, words;
     int pool;               // 0 col, 1 rowptr, 2 bitmap (host pools); 3 = the other arena (device copy)
@@ -241,8 +249,9 @@ enum BlockPart { kPartCol = 0, kPartRp = 1, kPartBm = 2, kPartTCol = 3, kPartTPo
 struct Wave {
     std::vector<StagedBlock> copies;
     uint64_t words = 0;         // arena words used
-    uint64_t rows = 0;          // implicit items (rows of its pieces)
-    size_t piece_begin = 0, piece_end = 0;   // range in the handle's wave piece table
+    size_t piece_begin = 0, piece_end = 0;   // range of owned pieces (locality order positions)
+    uint64_t item_begin = 0, item_end = 0;   // its heavy row items (the build's item list)
+    uint64_t light_begin = 0, light_end = 0; // its light row items
     size_t task_table = 0;      // index of this wave's TaskDev table (ntasks entries)
 };
 
@@ -291,6 +300,9 @@ struct pgabb_blocks_s {
     uint64_t n_items = 0;
     pgabb::DBuf<uint4> d_light;                      // light row items (thread per row, DESIGN R20)
     uint64_t n_light = 0;
+    // item offsets per owned piece in locality order (size pieces + 1): the waves of
+    // streaming residency take contiguous ranges of them
+    std::vector<uint64_t> piece_item_off, piece_light_off;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
 
@@ -298,11 +310,13 @@ struct pgabb_blocks_s {
     bool streaming = false;
     uint64_t max_task_bytes = 0;
     std::vector<pgabb::Wave> waves;
-    pgabb::DBuf<pgabb::WavePiece> d_wave_pieces;
     pgabb::DBuf<pgabb::TaskDev> d_wave_tasks;         // waves x ntasks, offsets relative to an arena
     pgabb::DBuf<uint32_t> d_arena[2];
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+    // PGABB_COUNT_TRACE: 4 timing events per wave (copy start/end, compute start/end)
+    std::vector<cudaEvent_t> trace_ev;
+    bool trace_valid = false;
     pgabb::HBuf<unsigned long long> h_result;        // pinned landing slot for the count
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev_mid = nullptr;
@@ -339,6 +353,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
                          unsigned long long* d_tv_out = nullptr, unsigned long long* d_cycles = nullptr,
                          int vm = 3);
 void task_times(pgabb_blocks_s* h, uint64_t* ns);
+void wave_trace(pgabb_blocks_s* h, double* out, uint64_t* nwaves);
 void connected_components(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, uint32_t* labels, uint64_t* ncomp,
                           uint32_t* iters);
 void local_clustering(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, const uint64_t* tv, double* cc);

@@ -79,6 +79,32 @@ def test_c5_streamed_out_of_core():
     assert T == GOLDEN["c5"]["triangles"]
 
 
+def test_two_c5_copies_streamed_beyond_c5():
+    # NEXT-2 at twice C5's size: the disjoint union of C5 and
+    # a relabelled copy -- n = 2^27, |E| = 2 x 2,078,644,777 = 4.16e9 edges -- built
+    # from host tuples (chunked upload, 64-bit edge offsets), kept in pinned host DRAM
+    # and counted through a 32 GiB device budget, about half the ~60 GB of blocks.
+    # Exact pin without the oracle: disjoint-union additivity, T = 2 T(C5) (golden).
+    cfg = CONFIGS["c5"]
+    n, s, d = cfg.generate()
+    s2 = np.concatenate([s, s + np.uint32(n)])
+    del s
+    d2 = np.concatenate([d, d + np.uint32(n)])
+    del d
+    with pg.build_blocks(2 * n, s2, d2, p=cfg.p, residency=pg.RESIDENT_HOST,
+                         device_budget_bytes=32 << 30) as b:
+        del s2, d2
+        st = b.stats()
+        assert st["m_edges"] == 2 * GOLDEN["c5"]["m_edges"]
+        assert st["block_bytes"] > 32 << 30
+        assert st["waves"] > 1
+        T = b.triangle_count(trace=True)
+        assert T == 2 * GOLDEN["c5"]["triangles"]
+        tr = b.wave_trace()
+        assert tr.shape == (st["waves"], 4)
+        assert (tr[:, 1] <= tr[:, 2] + 1e-3).all()        # a wave computes after its copy
+
+
 def test_c2_per_vertex_and_clustering_full():
     # NEXT-1 at the bench's c2 size: every t(v) and cc(v) against the oracle
     cfg = CONFIGS["c2"]

@@ -108,7 +108,13 @@ def test_streaming(orient):
     with pg.build_blocks(*g, p=8, orient=orient) as ref:
         mt = ref.stats()["max_task_bytes"]
     with pg.build_blocks(*g, p=8, orient=orient, residency=pg.RESIDENT_HOST, device_budget_bytes=3 * mt) as b:
-        assert b.stats()["waves"] > 1
+        nw = b.stats()["waves"]
+        assert nw > 1
+        assert b.triangle_count(trace=True) == T0
+        tr = b.wave_trace()                                  # copy/compute timeline (S9)
+        assert tr.shape == (nw, 4)
+        assert (tr[:, 0] <= tr[:, 1]).all() and (tr[:, 2] <= tr[:, 3]).all()
+        assert (tr[:, 1] <= tr[:, 2] + 1e-3).all()           # each wave computes after its copy
         assert b.triangle_count() == T0
         tv, _ = b.vertex_triangles()
         assert np.array_equal(tv, tv0)
