@@ -66,10 +66,9 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     h_rowptr.release();
     h_bitmap.release();
     d_wave_tasks.release();
-    d_arena[0].release();
-    d_arena[1].release();
-    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_done[0], ev_done[1]})
-        if (e) cudaEventDestroy(e);
+    d_arena.release();
+    for (cudaEvent_t e : ev_copied) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     d_bitmap.release();
     d_tasks.release();
@@ -164,7 +163,9 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         if (h->streaming) {
             plan_waves(h);
             PG_CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-            for (int a = 0; a < 2; ++a) {
+            h->ev_copied.assign(h->waves.size(), nullptr);
+            h->ev_done.assign(h->waves.size(), nullptr);
+            for (size_t a = 0; a < h->waves.size(); ++a) {
                 PG_CK(cudaEventCreateWithFlags(&h->ev_copied[a], cudaEventDisableTiming));
                 PG_CK(cudaEventCreateWithFlags(&h->ev_done[a], cudaEventDisableTiming));
             }

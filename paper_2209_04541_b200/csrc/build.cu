@@ -46,6 +46,7 @@ inline int bits_for(uint64_t x) {
     return b;
 }
 
+constexpr int kMaxSlots = 4;                       // streaming arena slots (block cache depth)
 constexpr uint64_t kUploadChunk = 1ull << 27;   // host tuples per staging chunk (1 GiB of u32 pairs)
 constexpr uint64_t kMidSaving = 2;   // R25 auto: saved streamed ids per visit needed for MID
 
@@ -1145,25 +1146,54 @@ static std::vector<size_t> locality_order(const pgabb_blocks_s* h) {
 // and its own task-descriptor table.  EBUDGET if one task's three blocks alone
 // exceed half the budget ("hard error").
 void plan_waves(pgabb_blocks_s* h) {
-    const uint64_t half = h->budget / 2 / 4;   // words per arena
+    // The device budget is one arena of K slots (a block cache deeper than double
+    // buffering, NEXT-2): wave k stages the parts it lacks into slot k mod K while
+    // wave k-1 computes.  A part that a recent wave already staged is read IN PLACE
+    // when its slot cannot be overwritten before this wave ends (the slots of waves
+    // k-1 .. k-K+2), copied device-to-device from the slot of wave k-K+1 (which wave
+    // k+1 overwrites while wave k runs), else copied from pinned host memory.  K is
+    // the largest of 4, 3, 2 whose slot holds the biggest task's parts.
+    const uint64_t budget_words = h->budget / 4;
     const size_t nt = h->tasks.size();
+    uint64_t max_task_words = 1;
+    for (const Task& T : h->tasks) {
+        PartRef parts[8];
+        const int np = task_parts(h, T, parts);
+        uint64_t wds = 0;
+        for (int q = 0; q < np; ++q) wds += part_words(h, parts[q]);
+        max_task_words = std::max(max_task_words, wds);
+    }
+    int K = 2;
+    for (int k = kMaxSlots; k > 2; --k)
+        if (max_task_words <= budget_words / k - kColPad) {
+            K = k;
+            break;
+        }
+    const uint64_t slot_words = budget_words / K - kColPad;
+    h->slots = K;
+    h->slot_words = slot_words;
     h->waves.clear();
     size_t npieces = 0;                 // owned pieces placed so far (locality order)
     std::vector<TaskDev> wtasks;
     const std::vector<size_t> order = locality_order(h);
-    // (block, part) -> arena word offset of the current wave
-    std::map<std::pair<uint32_t, int>, uint64_t> placed;
-    // the previous wave's placement: a block part it holds is copied device-to-device
-    // from the other arena instead of host-to-device (consecutive waves share blocks
-    // by the locality order: NEXT-2 block reuse)
-    std::map<std::pair<uint32_t, int>, uint64_t> prev_placed;
+    using Key = std::pair<uint32_t, int>;
+    struct Slot {
+        std::map<Key, uint64_t> parts;  // part -> absolute arena word offset
+        int64_t filled_by = -1, last_reader = -1;
+    };
+    std::vector<Slot> slot(K);
     Wave cur;
+    int64_t k = 0;                      // index of the wave being planned
     std::vector<TaskDev> cur_tasks;
     auto open_wave = [&]() {
         cur = Wave{};
         cur.piece_begin = npieces;
-        prev_placed.swap(placed);
-        placed.clear();
+        cur.slot = (int)(k % K);
+        Slot& sl = slot[cur.slot];
+        cur.wait_wave = sl.last_reader;  // the slot's previous readers must be done
+        sl.parts.clear();
+        sl.filled_by = k;
+        sl.last_reader = k;
         cur_tasks.assign(nt, TaskDev{});
     };
     auto close_wave = [&]() {
@@ -1176,10 +1206,26 @@ void plan_waves(pgabb_blocks_s* h) {
         cur.task_table = h->waves.size();
         wtasks.insert(wtasks.end(), cur_tasks.begin(), cur_tasks.end());
         h->waves.push_back(cur);
+        ++k;
+    };
+    // where a part can be read from for wave k without staging it: its own slot, or
+    // a slot of waves k-1 .. k-K+2 (not overwritten before wave k ends)
+    auto in_place = [&](const Key& key, int* from) -> const uint64_t* {
+        for (int s2 = 0; s2 < K; ++s2) {
+            const Slot& sl = slot[s2];
+            const bool ok = s2 == cur.slot || (sl.filled_by >= k - (K - 2) && sl.filled_by <= k - 1);
+            if (!ok) continue;
+            const auto it = sl.parts.find(key);
+            if (it != sl.parts.end()) {
+                *from = s2;
+                return &it->second;
+            }
+        }
+        return nullptr;
     };
     open_wave();
-    for (size_t k : order) {
-        const PieceDev& w = h->work[k];
+    for (size_t q0 : order) {
+        const PieceDev& w = h->work[q0];
         const Task& T = h->tasks[w.task];
         PartRef parts[8];
         const int np = task_parts(h, T, parts);
@@ -1187,41 +1233,57 @@ void plan_waves(pgabb_blocks_s* h) {
         for (int q = 0; q < np; ++q) {
             const uint64_t wd = part_words(h, parts[q]);
             all += wd;
-            if (!placed.count({parts[q].block, parts[q].part})) fresh += wd;
+            int from = 0;
+            if (!in_place({parts[q].block, parts[q].part}, &from)) fresh += wd;
         }
-        if (all > half)
+        if (all > slot_words)
             fail(PGABB_EBUDGET, "task (" + std::to_string(T.i) + "," + std::to_string(T.j) + "," +
                                     std::to_string(T.x) + ") needs " + std::to_string(all * 4) +
                                     " bytes of blocks, more than half the device budget");
-        if (cur.words + fresh > half) {
+        // pipeline ramp: the first waves are smaller (1/4, 1/2 of a slot) so the copy
+        // that no computation can hide is short
+        const uint64_t cap = k < 2 ? std::max<uint64_t>(slot_words >> (2 - k), all) : slot_words;
+        if (cur.words + fresh > cap && npieces > cur.piece_begin) {
             close_wave();
             open_wave();
         }
+        const uint64_t slot_base = (uint64_t)cur.slot * (slot_words + kColPad);
         for (int q = 0; q < np; ++q) {
-            const std::pair<uint32_t, int> key{parts[q].block, parts[q].part};
-            if (placed.count(key)) continue;
+            const Key key{parts[q].block, parts[q].part};
+            int from = 0;
+            if (const uint64_t* at = in_place(key, &from)) {
+                if (from != cur.slot) slot[from].last_reader = k;   // read in place by this wave
+                continue;
+            }
             const uint64_t wd = part_words(h, parts[q]);
+            const uint64_t dst = slot_base + cur.words;
+            // the slot of wave k-K+1 is overwritten by wave k+1: copy from it device-to-device
+            int64_t d2d_src = -1;
+            for (int s2 = 0; s2 < K; ++s2)
+                if (s2 != cur.slot && slot[s2].filled_by == k - (K - 1)) {
+                    const auto it = slot[s2].parts.find(key);
+                    if (it != slot[s2].parts.end()) d2d_src = (int64_t)it->second;
+                }
             int pool = 0;
             const uint64_t src = part_src(h, parts[q], &pool);
-            placed[key] = cur.words;
-            const auto pv = prev_placed.find(key);
-            if (wd && pv != prev_placed.end()) cur.copies.push_back(StagedBlock{pv->second, cur.words, wd, 3});
-            else if (wd) cur.copies.push_back(StagedBlock{src, cur.words, wd, pool});
+            if (wd && d2d_src >= 0) cur.copies.push_back(StagedBlock{(uint64_t)d2d_src, dst, wd, 3});
+            else if (wd) cur.copies.push_back(StagedBlock{src, dst, wd, pool});
+            slot[cur.slot].parts[key] = dst;
             cur.words += wd;
         }
-        cur_tasks[w.task] = make_taskdev(h, T, [&](PartRef r) { return placed[{r.block, r.part}]; });
+        cur_tasks[w.task] = make_taskdev(h, T, [&](PartRef r) {
+            int from = 0;
+            return *in_place({r.block, r.part}, &from);
+        });
         ++npieces;
     }
     close_wave();
     h->d_wave_tasks.alloc(std::max<size_t>(wtasks.size(), 1));
     if (!wtasks.empty())
         PG_COPY_SYNC(h->d_wave_tasks.p, wtasks.data(), wtasks.size() * sizeof(TaskDev), h->stream);
-    uint64_t maxw = 1;
-    for (const Wave& wv : h->waves) maxw = std::max(maxw, wv.words);
-    for (int a = 0; a < 2; ++a) {   // padded like the col pool (16-byte list covers)
-        h->d_arena[a].alloc(maxw + kColPad);
-        PG_CK(cudaMemsetAsync(h->d_arena[a].p + maxw, 0, kColPad * 4, h->stream));
-    }
+    // one arena of K slots, each padded like the col pool (16-byte list covers)
+    h->d_arena.alloc((uint64_t)K * (slot_words + kColPad));
+    PG_CK(cudaMemsetAsync(h->d_arena.p, 0, h->d_arena.bytes(), h->stream));
 }
 
 // This rank's work list: owned pieces in (task, row) order, the task descriptors

@@ -1163,27 +1163,26 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         h->trace_valid = trace;
         for (size_t k = 0; k < h->waves.size(); ++k) {
             const Wave& wv = h->waves[k];
-            const int a = (int)(k & 1);
-            if (k >= 2) PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev_done[a], 0));
+            if (wv.wait_wave >= 0) PG_CK(cudaStreamWaitEvent(h->copy_stream, h->ev_done[wv.wait_wave], 0));
             if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k], h->copy_stream));
             for (const StagedBlock& c : wv.copies) {
-                if (c.pool == 3) {   // held by the previous wave: device-to-device from the other arena
-                    PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, h->d_arena[1 - a].p + c.src_word,
+                if (c.pool == 3) {   // staged by the wave k-K+1: device-to-device within the arena
+                    PG_CK(cudaMemcpyAsync(h->d_arena.p + c.dst_word, h->d_arena.p + c.src_word,
                                           c.words * 4, cudaMemcpyDeviceToDevice, h->copy_stream));
                     h->d2d_last += c.words * 4;
                     continue;
                 }
-                PG_CK(cudaMemcpyAsync(h->d_arena[a].p + c.dst_word, pools[c.pool] + c.src_word, c.words * 4,
+                PG_CK(cudaMemcpyAsync(h->d_arena.p + c.dst_word, pools[c.pool] + c.src_word, c.words * 4,
                                       cudaMemcpyHostToDevice, h->copy_stream));
                 h->h2d_last += c.words * 4;
             }
-            PG_CK(cudaEventRecord(h->ev_copied[a], h->copy_stream));
+            PG_CK(cudaEventRecord(h->ev_copied[k], h->copy_stream));
             if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 1], h->copy_stream));
-            PG_CK(cudaStreamWaitEvent(st, h->ev_copied[a], 0));
+            PG_CK(cudaStreamWaitEvent(st, h->ev_copied[k], 0));
             if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 2], st));
             // the wave's ranges of the row items; its task table and all three pool
             // pointers address the arena
-            const uint32_t* base = h->d_arena[a].p;
+            const uint32_t* base = h->d_arena.p;
             const TaskDev* wt = h->d_wave_tasks.p + wv.task_table * nt;
             PG_CK(cudaMemsetAsync(h->d_next.p + 2, 0, 2 * sizeof(unsigned long long), st));
             if (wv.item_end > wv.item_begin) {
@@ -1202,7 +1201,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
                 PG_LAUNCH_CHECK();
                 h->launches_last++;
             }
-            PG_CK(cudaEventRecord(h->ev_done[a], st));
+            PG_CK(cudaEventRecord(h->ev_done[k], st));
             if (trace) PG_CK(cudaEventRecord(h->trace_ev[4 * k + 3], st));
         }
     }

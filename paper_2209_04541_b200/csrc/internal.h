@@ -247,8 +247,10 @@ struct StagedBlock {        // one H2D copy: pool range -> arena offset (u32 wor
 enum BlockPart { kPartCol = 0, kPartRp = 1, kPartBm = 2, kPartTCol = 3, kPartTPos = 4, kPartTRp = 5 };
 
 struct Wave {
-    std::vector<StagedBlock> copies;
-    uint64_t words = 0;         // arena words used
+    std::vector<StagedBlock> copies;   // dst_word: absolute arena offset; pool 3: src in the arena
+    int slot = 0;               // arena slot this wave stages into
+    int64_t wait_wave = -1;     // wave whose end must precede this wave's copies (slot reuse)
+    uint64_t words = 0;         // slot words used
     size_t piece_begin = 0, piece_end = 0;   // range of owned pieces (locality order positions)
     uint64_t item_begin = 0, item_end = 0;   // its heavy row items (the build's item list)
     uint64_t light_begin = 0, light_end = 0; // its light row items
@@ -311,9 +313,11 @@ struct pgabb_blocks_s {
     uint64_t max_task_bytes = 0;
     std::vector<pgabb::Wave> waves;
     pgabb::DBuf<pgabb::TaskDev> d_wave_tasks;         // waves x ntasks, offsets relative to an arena
-    pgabb::DBuf<uint32_t> d_arena[2];
+    pgabb::DBuf<uint32_t> d_arena;                    // slots x (slot_words + pad)
+    int slots = 0;
+    uint64_t slot_words = 0;
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_copied, ev_done;       // per wave (streaming)
     // PGABB_COUNT_TRACE: 4 timing events per wave (copy start/end, compute start/end)
     std::vector<cudaEvent_t> trace_ev;
     bool trace_valid = false;
