@@ -53,6 +53,9 @@ def parse(argv=None):
     ap.add_argument("--budget-gb", type=float, default=0.0,
                     help="> 0: blocks stay in pinned host memory and each count streams them through "
                          "a device budget of this many GB (S9 out-of-core mode, PAPER.md:829-835)")
+    ap.add_argument("--host-permille", type=int, default=0,
+                    help="> 0: collaborative CPU + GPU (NEXT-3) -- blocks in pinned host memory, the "
+                         "sparsest pieces up to this share of the cost counted by host threads")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="flow tests only: allow more ranks than visible GPUs (ranks share a GPU, gloo)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -498,7 +501,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e and not vertex and args.budget_gb <= 0:
         bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
-                             residency=pg.RESIDENT_HOST,
+                             residency=pg.RESIDENT_HOST, host_permille=args.host_permille,
                              task_weights=getattr(b, "task_weights_used", None))
         for _ in range(max(1, args.warmup)):
             bh.triangle_count()
@@ -521,6 +524,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(sh["h2d_bytes_last"]), "d2h_bytes_per_step": 8,
                "ms_per_step": 1e3 * e_s, "timer": "host wall clock around the public call, median of steps, "
                                                  "max over ranks"}
+        if args.host_permille:   # NEXT-3: sparsest pieces counted by host threads (no H2D for them)
+            e2e["host_permille"] = args.host_permille
+            e2e["ms_host_share"] = float(sh["ms_host_last"])
         bh.free()
 
     cpu = None

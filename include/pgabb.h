@@ -115,7 +115,16 @@ typedef struct {
                                    ids w > v of A_ix[u] for every (u,v) in A_ij (needs the
                                    blocks' transposes: 2 more u32 per edge).  Counts are
                                    identical for every value. */
-    uint32_t reserved0;
+    uint32_t host_permille;     /* collaborative CPU + GPU (PAPER.md:193-198,
+                                   840-849: sparse tasks "more successful by assigning them to
+                                   CPUs"): with PGABB_RESIDENT_HOST and no budget, this rank's
+                                   sparsest pieces (least S7 cost per edge first) up to this
+                                   share (per mille) of its cost are counted by host threads
+                                   from the pinned host blocks while the GPU counts the rest;
+                                   their blocks are not copied.  0 = GPU only (default).
+                                   EINVAL with another residency, a budget, or > 1000.  Counts
+                                   are unchanged; per-vertex counts and task times need 0. */
+    uint32_t host_threads;      /* host threads for host_permille (0 = all hardware threads) */
 } pgabb_build_opts_t;
 
 #define PGABB_ORIENT_AUTO 0u
@@ -237,7 +246,8 @@ typedef struct {
     double ms_main_kernel_last;         /* device time of the intersection kernels (heavy + light) */
     double ms_light_kernel_last;        /* device time of the light-row kernel alone */
     double ms_cc_last;                  /* device time of the last pgabb_connected_components */
-    double reserved_d[1];
+    double ms_host_last;                /* host_permille > 0: wall time of the host threads' share
+                                           of the last count (runs concurrently with the GPU) */
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);

@@ -143,6 +143,11 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         h->reverse_order = o.reverse_order;
         if (o.orient > PGABB_ORIENT_MID) fail(PGABB_EINVAL, "orient must be 0 (auto), 1 (low) or 2 (mid)");
         h->orient = o.orient;
+        if (o.host_permille > 1000) fail(PGABB_EINVAL, "host_permille must be <= 1000");
+        if (o.host_permille && (o.residency != PGABB_RESIDENT_HOST || o.device_budget_bytes))
+            fail(PGABB_EINVAL, "host_permille needs PGABB_RESIDENT_HOST without a device budget");
+        h->host_permille = o.host_permille;
+        h->host_threads = o.host_threads;
         h->budget = o.device_budget_bytes;
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
         if (o.task_weights) h->task_weights.assign(o.task_weights, o.task_weights + o.n_task_weights);
@@ -214,6 +219,7 @@ pgabb_status_t pgabb_vertex_triangles(pgabb_blocks_t b, const pgabb_count_opts_t
             fail(PGABB_EINVAL, "PGABB_OUT_ACCUMULATE needs PGABB_OUT_DEVICE");
         if (opts && (opts->flags & PGABB_COUNT_ASYNC) && !(opts->flags & PGABB_OUT_DEVICE))
             fail(PGABB_EINVAL, "PGABB_COUNT_ASYNC needs PGABB_OUT_DEVICE (a host tv is written synchronously)");
+        if (!b->host_work.empty()) fail(PGABB_EINVAL, "per-vertex counts need host_permille 0");
         DeviceGuard g(b->device);
         const bool on_dev = opts && (opts->flags & PGABB_OUT_DEVICE);
         DBuf<unsigned long long> tmp;
@@ -253,6 +259,7 @@ pgabb_status_t pgabb_task_times(pgabb_blocks_t b, uint64_t* ns) {
     return guarded([&] {
         if (!b || !ns) fail(PGABB_EINVAL, "NULL argument");
         if (b->streaming) fail(PGABB_EINVAL, "task times are measured on a device-resident handle");
+        if (!b->host_work.empty()) fail(PGABB_EINVAL, "task times need host_permille 0");
         DeviceGuard g(b->device);
         task_times(b, ns);
     });
@@ -300,6 +307,7 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->ms_main_kernel_last = b->ms_main_last;
         s->ms_light_kernel_last = b->ms_light_last;
         s->ms_cc_last = b->ms_cc_last;
+        s->ms_host_last = b->ms_host_last;
         s->items_heavy = b->n_items;
         s->items_light = b->n_light;
         s->alg_bytes_light = b->alg_light;

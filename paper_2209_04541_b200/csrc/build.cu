@@ -1324,6 +1324,46 @@ void upload_work(pgabb_blocks_s* h) {
         h->cost_local += pc.cost;
         task_mine[pc.task] = 1;
     }
+    // NEXT-3 collaborative CPU + GPU: the sparsest owned
+    // pieces -- least S7 cost per neighbour visit, the latency-bound ones the paper
+    // sends to CPUs -- up to host_permille of this rank's cost are counted by host
+    // threads from the pinned host pools; the GPU neither copies nor counts them
+    h->host_work.clear();
+    h->host_tasks.clear();
+    if (h->host_permille && !h->work.empty()) {
+        std::vector<size_t> byd(h->work.size());
+        std::iota(byd.begin(), byd.end(), 0);
+        auto pcost = [&](const PieceDev& w) {   // the piece's S7 cost (its Piece record)
+            for (const Piece& pc : h->pieces)
+                if (pc.task == w.task && pc.r0 == w.r0 && pc.owner == me) return pc.rcost;
+            return (uint64_t)0;
+        };
+        std::vector<uint64_t> cst(h->work.size());
+        for (size_t q = 0; q < h->work.size(); ++q) cst[q] = pcost(h->work[q]);
+        std::stable_sort(byd.begin(), byd.end(), [&](size_t a, size_t b) {
+            // cost per visit ascending: cst[a]/visits[a] < cst[b]/visits[b]
+            const unsigned __int128 l = (unsigned __int128)cst[a] * (h->work[b].e1 - h->work[b].e0);
+            const unsigned __int128 r = (unsigned __int128)cst[b] * (h->work[a].e1 - h->work[a].e0);
+            return l < r;
+        });
+        uint64_t total = 0;
+        for (uint64_t c : cst) total += c;
+        const unsigned __int128 want = (unsigned __int128)total * h->host_permille;
+        std::vector<char> to_host(h->work.size(), 0);
+        unsigned __int128 got = 0;
+        for (size_t q : byd) {
+            if (got * 1000 >= want) break;
+            to_host[q] = 1;
+            got += cst[q];
+        }
+        std::vector<PieceDev> gpu;
+        for (size_t q = 0; q < h->work.size(); ++q) (to_host[q] ? h->host_work : gpu).push_back(h->work[q]);
+        h->work.swap(gpu);
+        h->host_tasks = td;
+        h->h_host_counts.alloc(std::max<size_t>(h->tasks.size(), 1));
+        h->d_host_counts.alloc(std::max<size_t>(h->tasks.size(), 1));
+    }
+
     // staged-model bytes of the owned pieces: whole tasks are attributed to the
     // rank that owns their first piece's share in proportion to cost
     for (size_t t = 0; t < h->tasks.size(); ++t) {

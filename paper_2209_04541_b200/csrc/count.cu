@@ -8,6 +8,9 @@
 // sorted-set intersection; "list or hashmap-based" leaves
 // the method open (DESIGN R8).
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
 
 #include "internal.h"
 
@@ -1036,6 +1039,88 @@ extern "C" PGABB_API int pgabb_prof_read(unsigned long long* out, int reset) {
 namespace pgabb {
 #endif
 
+// ---- NEXT-3 collaborative CPU + GPU: the host threads' share ------------------
+// Same sums as the kernels (Listing 5), in the task's
+// orientation (TaskDev roles, R25), read from the pinned host pools: per row r the
+// held list S against every neighbour's streamed list, by a merge (or a binary
+// search of the shorter list's ids in the longer one when their sizes are skewed).
+static uint64_t host_intersect(const uint32_t* a, uint32_t la, const uint32_t* b, uint32_t lb) {
+    if (la == 0 || lb == 0) return 0;
+    if (la > lb) {
+        std::swap(a, b);
+        std::swap(la, lb);
+    }
+    uint64_t c = 0;
+    if ((uint64_t)la * 16 < lb) {   // skewed: binary search, window shrinking
+        const uint32_t* lo = b;
+        const uint32_t* end = b + lb;
+        for (uint32_t i = 0; i < la && lo < end; ++i) {
+            lo = std::lower_bound(lo, end, a[i]);
+            if (lo < end && *lo == a[i]) ++c;
+        }
+        return c;
+    }
+    uint32_t i = 0, j = 0;
+    while (i < la && j < lb) {
+        const uint32_t x = a[i], y = b[j];
+        c += (x == y);
+        i += (x <= y);
+        j += (y <= x);
+    }
+    return c;
+}
+
+static void host_count_share(pgabb_blocks_s* h, unsigned long long* per_task) {
+    const uint32_t* col = h->h_col.p;
+    const uint32_t* rp = h->h_rowptr.p;
+    struct Unit { uint32_t piece, r0, r1; };
+    std::vector<Unit> units;
+    for (uint32_t k = 0; k < h->host_work.size(); ++k) {
+        const PieceDev& w = h->host_work[k];
+        for (uint32_t r = w.r0; r < w.r1; r += 4096) units.push_back(Unit{k, r, std::min(w.r1, r + 4096)});
+    }
+    const size_t nt = h->tasks.size();
+    unsigned nthr = h->host_threads ? h->host_threads : std::max(1u, std::thread::hardware_concurrency());
+    nthr = (unsigned)std::min<size_t>(nthr, std::max<size_t>(units.size(), 1));
+    std::atomic<size_t> next{0};
+    std::vector<std::vector<unsigned long long>> part(nthr, std::vector<unsigned long long>(nt, 0));
+    auto worker = [&](unsigned id) {
+        std::vector<unsigned long long>& acc = part[id];
+        for (size_t q; (q = next.fetch_add(1)) < units.size();) {
+            const Unit& un = units[q];
+            const PieceDev& w = h->host_work[un.piece];
+            const TaskDev& T = h->host_tasks[w.task];
+            uint64_t c = 0;
+            for (uint32_t r = un.r0; r < un.r1; ++r) {
+                const uint32_t a0 = rp[T.s_rp + r], la = rp[T.s_rp + r + 1] - a0;
+                const uint32_t e0 = rp[T.n_rp + r], e1 = rp[T.n_rp + r + 1];
+                if (la == 0) continue;
+                const uint32_t* A = col + T.s_col + a0;
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t nb = col[T.n_col + e];
+                    const uint32_t b1 = rp[T.t_rp + nb + 1];
+                    const uint32_t b0 = T.n_pos != ~0ull ? col[T.n_pos + e] + 1 : rp[T.t_rp + nb];
+                    if (b1 > b0) c += host_intersect(A, la, col + T.t_col + b0, b1 - b0);
+                }
+            }
+            acc[w.task] += c;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nthr; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (std::thread& th : pool) th.join();
+    for (size_t t = 0; t < nt; ++t) {
+        unsigned long long s = 0;
+        for (unsigned id = 0; id < nthr; ++id) s += part[id][t];
+        per_task[t] = s;
+    }
+}
+
+__global__ void k_add_counts(unsigned long long* tc, const unsigned long long* add, int nt) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) tc[t] += add[t];
+}
+
 uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool* wrote,
                          unsigned long long* d_tv_out, unsigned long long* d_cycles, int vm) {
     const bool timed = d_cycles != nullptr;   // pgabb_task_times: counting kernels with cycle accounting
@@ -1206,6 +1291,19 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
     }
     PG_CK(cudaEventRecord(h->ev2, st));
+    h->ms_host_last = 0;
+    if (!h->host_work.empty()) {
+        // NEXT-3: the host share runs now, while the GPU works through the copies and
+        // kernels enqueued above; its per-task counts join the device's before the sum
+        const auto t0 = std::chrono::steady_clock::now();
+        host_count_share(h, h->h_host_counts.p);
+        h->ms_host_last = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        PG_CK(cudaMemcpyAsync(h->d_host_counts.p, h->h_host_counts.p, nt * sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, st));
+        k_add_counts<<<(nt + 255) / 256, 256, 0, st>>>(h->d_task_counts.p, h->d_host_counts.p, nt);
+        PG_LAUNCH_CHECK();
+        h->launches_last++;
+    }
     k_sum_tasks<<<1, 1024, 0, st>>>(h->d_task_counts.p, nt, (unsigned long long*)(opts ? opts->d_count : nullptr));
     PG_LAUNCH_CHECK();
     h->launches_last++;

@@ -294,9 +294,17 @@ struct pgabb_blocks_s {
     // blocks only other ranks' pieces need
     std::vector<pgabb::StagedBlock> host_copies;
 
-    // this rank's work list
+    // this rank's work list (GPU pieces)
     std::vector<pgabb::PieceDev> work;
     uint64_t work_edges = 0;
+    // collaborative CPU + GPU (NEXT-3): this rank's pieces counted by host threads from
+    // the pinned host pools, with their task descriptors (host pool offsets)
+    uint32_t host_permille = 0, host_threads = 0;
+    std::vector<pgabb::PieceDev> host_work;
+    std::vector<pgabb::TaskDev> host_tasks;
+    pgabb::HBuf<unsigned long long> h_host_counts;   // per task, pinned (H2D into the device counts)
+    pgabb::DBuf<unsigned long long> d_host_counts;
+    double ms_host_last = 0;
     pgabb::DBuf<pgabb::TaskDev> d_tasks;             // ntasks descriptors
     pgabb::DBuf<unsigned long long> d_items;         // heavy row items (warp per row)
     uint64_t n_items = 0;

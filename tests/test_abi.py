@@ -48,7 +48,7 @@ def test_binding_matches_header():
 
 def test_struct_layouts():
     from paper_2209_04541_b200 import _abi
-    assert ctypes.sizeof(_abi.BuildOpts) == 64
+    assert ctypes.sizeof(_abi.BuildOpts) == 72
     assert ctypes.sizeof(_abi.CountOpts) == 32
     assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # + ms_cc_last took a reserved double   # 17 counters + items_heavy/light, alg_bytes_light, d2d_bytes_last; 6 doubles
 
