@@ -213,12 +213,25 @@ def cpu_baseline(cfg_name, n, s, d, target_s):
     T_s, e_s = g.count_range(0, n, stride)
     dt = time.perf_counter() - t0
     m_edges = g.m_edges
+    single = None
+    if cfg_name in ("c1", "c2"):
+        # the same count on ONE host thread (C1 and C2 also single-threaded)
+        ncores = oracle.threads()
+        oracle.set_threads(1)
+        t1 = time.perf_counter()
+        T1, e1 = g.count_range(0, n, stride)
+        d1 = time.perf_counter() - t1
+        oracle.set_threads(ncores)
+        single = {"value": e1 / d1, "unit": UNIT, "cores": 1, "seconds": d1, "triangles_in_sample": T1}
     g.close()
     sample = ("full graph" if stride == 1 else
               f"every {stride}-th vertex as the lowest triangle vertex ({e_s} of {m_edges} DAG edges)")
-    return {"value": e_s / dt, "unit": UNIT, "cores": oracle.threads(), "cpu_model": cpu_model(), "kind": "oracle",
-            "sample": f"{cfg_name}: node iterator over {sample}; oracle build {t_build:.1f}s excluded",
-            "seconds": dt, "triangles_in_sample": T_s, "full": stride == 1}
+    out = {"value": e_s / dt, "unit": UNIT, "cores": oracle.threads(), "cpu_model": cpu_model(), "kind": "oracle",
+           "sample": f"{cfg_name}: node iterator over {sample}; oracle build {t_build:.1f}s excluded",
+           "seconds": dt, "triangles_in_sample": T_s, "full": stride == 1}
+    if single:
+        out["single_thread"] = single
+    return out
 
 
 L2_NOTE = "L2 flushed (256 MiB write) between timed steps, outside the events"

@@ -110,6 +110,10 @@ constexpr uint32_t kDenseRowWideW = PGABB_DENSE_ROW_WIDE_W;
 #define PGABB_ROW_CHUNK 4
 #endif
 constexpr int kRowChunk = PGABB_ROW_CHUNK;   // row items per warp claim
+#ifndef PGABB_SMALL_HELD
+#define PGABB_SMALL_HELD 0   // A/B: c5 1.006 -> 1.043 s, c2 2.52 -> 2.59 ms with it (the flattened lists win)
+#endif
+constexpr bool kSmallHeld = PGABB_SMALL_HELD;   // heavy rows with <= kLightLa held ids: per-lane lists
 
 // Claims the next kRowChunk items for the calling warp; returns the first (>= n: done).
 __device__ __forceinline__ unsigned long long claim_items(unsigned long long* next, unsigned long long n, int lane,
@@ -528,6 +532,93 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
     return acc;
 }
 
+constexpr int kLightThreads = 256;
+#ifndef PGABB_LIGHT_MINB
+#define PGABB_LIGHT_MINB 6   // 6 x 256 threads per SM (40 registers, with the item prefetch): A/B best on c2/c3/c4
+#endif
+#ifndef PGABB_LIGHT_CHUNK
+#define PGABB_LIGHT_CHUNK 8
+#endif
+constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
+#ifndef PGABB_LIGHT_PREFETCH
+#define PGABB_LIGHT_PREFETCH 1
+#endif
+constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
+#ifndef PGABB_LIGHT_VPIPE
+#define PGABB_LIGHT_VPIPE 1
+#endif
+constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
+
+// The list branch of a light row: for each neighbour v (vcol[e0..e1)) its streamed
+// list Bc[b0..b1) -- from rowptr, or (POS: MID tasks with x == j) from after the
+// row vertex, npos[e] + 1 -- is scanned against the held ids a[] (<= kLightScan
+// ids) or binary-searched once per held id.  The next neighbour and its bounds are
+// loaded while the current list is scanned (PGABB_LIGHT_VPIPE).
+// LA: a bound on |held| for the whole warp (1, 2, 4 or kLightLa), so a scanned id
+// is compared with LA held slots, not kLightLa (unused slots are ~0u).
+// STRIDE: the thread takes neighbours e0, e0 + STRIDE, ... (1 in the light kernel;
+// 32 when the lanes of a warp share one row, the heavy kernel's small-held path).
+template <int VM, bool POS, int LA, int STRIDE = 1>
+__device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
+                                                const uint32_t* __restrict__ vcol, const uint32_t* __restrict__ npos,
+                                                uint64_t rp_jx, const uint32_t* __restrict__ Bc, uint32_t e0,
+                                                uint32_t e1, const uint32_t (&a)[kLightLa], uint32_t la,
+                                                unsigned long long* __restrict__ tvj,
+                                                unsigned long long* __restrict__ tvx) {
+    uint32_t acc = 0;
+    uint32_t vn = 0, bn0 = 0, bn1 = 0;
+    if (kLightVPipe && e0 < e1) {
+        vn = __ldg(vcol + e0);
+        bn0 = POS ? __ldg(npos + e0) + 1 : __ldg(rowptr + rp_jx + vn);
+        bn1 = __ldg(rowptr + rp_jx + vn + 1);
+    }
+    for (uint32_t e = e0; e < e1; e += STRIDE) {
+        uint32_t v, b0, b1;
+        if (kLightVPipe) {
+            v = vn;
+            b0 = bn0;
+            b1 = bn1;
+            if (e + STRIDE < e1) {
+                vn = __ldg(vcol + e + STRIDE);
+                bn0 = POS ? __ldg(npos + e + STRIDE) + 1 : __ldg(rowptr + rp_jx + vn);
+                bn1 = __ldg(rowptr + rp_jx + vn + 1);
+            }
+        } else {
+            v = __ldg(vcol + e);
+            b0 = POS ? __ldg(npos + e) + 1 : __ldg(rowptr + rp_jx + v);
+            b1 = __ldg(rowptr + rp_jx + v + 1);
+        }
+        const uint32_t lb = b1 - b0;
+        uint32_t c = 0;
+        if (lb <= kLightScan) {
+            for (uint32_t q = b0; q < b1; ++q) {
+                const uint32_t x = __ldg(Bc + q);
+                uint32_t hit = 0;
+#pragma unroll
+                for (int k = 0; k < LA; ++k) hit |= (x == a[k]);
+                if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
+                c += hit;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < LA; ++k)
+                if (k < (int)la) {
+                    uint32_t lo = b0, hi = b1;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
+                    }
+                    const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
+                    if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
+                    c += hit;
+                }
+        }
+        acc += c;
+        if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
+    }
+    return acc;
+}
+
 // items[] holds the row items in locality order: the whole rank's (device-resident
 // blocks) or one wave's range of them (streaming residency: the task table and the
 // pool pointers then all point at the wave's staging arena).
@@ -604,6 +695,25 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
             acc = probe_dense_row<VM>(vcol, e0, e1, A, la, bitmap + T.t_bm, T.bm_words, lane, tvj, tvx);
             PROF_MARK(1);
             PROF_CNT(16);
+        } else if (kSmallHeld && la <= kLightLa) {
+            // small held list (<= kLightLa ids, the MID rows of the low-degree part): no
+            // set staging -- every lane holds S in registers and takes every 32nd
+            // neighbour, scanning its (short) streamed list against S or binary-
+            // searching S's ids in a longer one (the light kernel's per-thread loop)
+            const uint32_t mine = lane < (int)la ? __ldg(A + lane) : 0xffffffffu;
+            uint32_t a[kLightLa];
+#pragma unroll
+            for (int k = 0; k < (int)kLightLa; ++k) a[k] = __shfl_sync(0xffffffffu, mine, k);
+#define SMALL(P, L)                                                                                          \
+    light_lists<VM, P, L, 32>(col, rowptr, vcol, npos, T.t_rp, Bc, e0 + lane, e1, a, la, tvj, tvx)
+            if (npos)
+                acc = la <= 1 ? SMALL(true, 1) : la <= 2 ? SMALL(true, 2) : la <= 4 ? SMALL(true, 4)
+                                                                             : SMALL(true, (int)kLightLa);
+            else
+                acc = la <= 1 ? SMALL(false, 1) : la <= 2 ? SMALL(false, 2) : la <= 4 ? SMALL(false, 4)
+                                                                               : SMALL(false, (int)kLightLa);
+#undef SMALL
+            PROF_MARK(5);
         } else if (mode == 0) {
             for (uint32_t k = lane; k < la; k += 32) {
                 const uint32_t w = __ldg(A + k);
@@ -761,91 +871,6 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
 // task changes.  Same exact |A_ix[u] ∩ A_jx[v]| sums as
 // k_tc_rows (Listing 5).
 // ---------------------------------------------------------------------------
-constexpr int kLightThreads = 256;
-#ifndef PGABB_LIGHT_MINB
-#define PGABB_LIGHT_MINB 6   // 6 x 256 threads per SM (40 registers, with the item prefetch): A/B best on c2/c3/c4
-#endif
-#ifndef PGABB_LIGHT_CHUNK
-#define PGABB_LIGHT_CHUNK 8
-#endif
-constexpr int kLightChunk = PGABB_LIGHT_CHUNK;   // items per lane per claim
-#ifndef PGABB_LIGHT_PREFETCH
-#define PGABB_LIGHT_PREFETCH 1
-#endif
-constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
-#ifndef PGABB_LIGHT_VPIPE
-#define PGABB_LIGHT_VPIPE 1
-#endif
-constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
-
-// The list branch of a light row: for each neighbour v (vcol[e0..e1)) its streamed
-// list Bc[b0..b1) -- from rowptr, or (POS: MID tasks with x == j) from after the
-// row vertex, npos[e] + 1 -- is scanned against the held ids a[] (<= kLightScan
-// ids) or binary-searched once per held id.  The next neighbour and its bounds are
-// loaded while the current list is scanned (PGABB_LIGHT_VPIPE).
-// LA: a bound on |held| for the whole warp (1, 2, 4 or kLightLa), so a scanned id
-// is compared with LA held slots, not kLightLa (unused slots are ~0u).
-template <int VM, bool POS, int LA>
-__device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
-                                                const uint32_t* __restrict__ vcol, const uint32_t* __restrict__ npos,
-                                                uint64_t rp_jx, const uint32_t* __restrict__ Bc, uint32_t e0,
-                                                uint32_t e1, const uint32_t (&a)[kLightLa], uint32_t la,
-                                                unsigned long long* __restrict__ tvj,
-                                                unsigned long long* __restrict__ tvx) {
-    uint32_t acc = 0;
-    uint32_t vn = 0, bn0 = 0, bn1 = 0;
-    if (kLightVPipe) {
-        vn = __ldg(vcol + e0);
-        bn0 = POS ? __ldg(npos + e0) + 1 : __ldg(rowptr + rp_jx + vn);
-        bn1 = __ldg(rowptr + rp_jx + vn + 1);
-    }
-    for (uint32_t e = e0; e < e1; ++e) {
-        uint32_t v, b0, b1;
-        if (kLightVPipe) {
-            v = vn;
-            b0 = bn0;
-            b1 = bn1;
-            if (e + 1 < e1) {
-                vn = __ldg(vcol + e + 1);
-                bn0 = POS ? __ldg(npos + e + 1) + 1 : __ldg(rowptr + rp_jx + vn);
-                bn1 = __ldg(rowptr + rp_jx + vn + 1);
-            }
-        } else {
-            v = __ldg(vcol + e);
-            b0 = POS ? __ldg(npos + e) + 1 : __ldg(rowptr + rp_jx + v);
-            b1 = __ldg(rowptr + rp_jx + v + 1);
-        }
-        const uint32_t lb = b1 - b0;
-        uint32_t c = 0;
-        if (lb <= kLightScan) {
-            for (uint32_t q = b0; q < b1; ++q) {
-                const uint32_t x = __ldg(Bc + q);
-                uint32_t hit = 0;
-#pragma unroll
-                for (int k = 0; k < LA; ++k) hit |= (x == a[k]);
-                if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
-                c += hit;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < LA; ++k)
-                if (k < (int)la) {
-                    uint32_t lo = b0, hi = b1;
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
-                    }
-                    const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
-                    if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
-                    c += hit;
-                }
-        }
-        acc += c;
-        if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
-    }
-    return acc;
-}
-
 // items: the whole rank's light items, or one wave's range of them (streaming: the
 // task table and pools then point at the wave's arena).
 template <int VM, bool TIMED>
