@@ -949,12 +949,13 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
 #define LLISTS(P, L)                                                                                       \
     light_lists<VM, P, L>(col, rowptr, col + col_ij, P ? col + npos : nullptr, T.t_rp, col + T.t_col, e0, e1, a, \
                           la, tvj, tvx)
+            constexpr int kLa8 = kLightLa > 8 ? 8 : (int)kLightLa;   // the 8-wide step when kLightLa > 8
             if (npos != ~0ull)
                 acc = lam <= 1 ? LLISTS(true, 1) : lam <= 2 ? LLISTS(true, 2) : lam <= 4 ? LLISTS(true, 4)
-                                                                                 : LLISTS(true, (int)kLightLa);
+                    : lam <= 8 ? LLISTS(true, kLa8) : LLISTS(true, (int)kLightLa);
             else
                 acc = lam <= 1 ? LLISTS(false, 1) : lam <= 2 ? LLISTS(false, 2) : lam <= 4 ? LLISTS(false, 4)
-                                                                                   : LLISTS(false, (int)kLightLa);
+                    : lam <= 8 ? LLISTS(false, kLa8) : LLISTS(false, (int)kLightLa);
 #undef LLISTS
         }
         acc_t += acc;

@@ -37,17 +37,19 @@ def run(names):
     lib = pg._lib
     lib.pgabb_prof_read.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     buf = (ctypes.c_uint64 * 32)()
-    for name in names:
+    for spec in names:
+        name, _, path = spec.partition(":")   # "c2" (count) or "c2:vertex" (per-vertex t(v), VM=3)
         cfg = CONFIGS[name]
         n, s, d = cfg.generate()
         with pg.build_blocks(n, s, d, p=cfg.p) as b:
-            b.triangle_count()
+            run1 = (lambda: int(b.vertex_triangles().sum()) // 3) if path == "vertex" else b.triangle_count
+            run1()
             lib.pgabb_prof_read(buf, 1)
-            T = b.triangle_count()
+            T = run1()
             ms = b.stats()["ms_main_kernel_last"]
             lib.pgabb_prof_read(buf, 1)
         tot = sum(buf[c] for c in range(10))
-        res = {"config": name, "triangles": T, "kernel_ms": ms,
+        res = {"config": spec, "triangles": T, "kernel_ms": ms,
                "share": {CATS[c]: round(buf[c] / max(tot, 1), 4) for c in range(10)},
                "counts": {CATS[c]: int(buf[c]) for c in range(16, 20)}}
         print(json.dumps(res), flush=True)
