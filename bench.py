@@ -366,30 +366,44 @@ def roofline_of(cfg_name, kernels, ms_step, peak, peak_src, vertex, sm_clock_mhz
         r["traffic"] = dram
         r["ncu"] = {k: nc.get(k) for k in ("source", "src_hash", "current", "l2_hit_pct", "issue_active_pct",
                                            "warp_inst_per_launch", "top_stall", "kernel_ms_under_ncu")}
+        # fractions from the capture itself (its DRAM bytes over its own kernel time, its
+        # issue-active ratio), so they stay consistent even when the capture is of an
+        # older build (ncu.current false); the live event time gives dram_gbs_live
         dfrac = ifrac = None
-        if dram is not None and dom["ms"] > 0:
-            dgbs = dram / (dom["ms"] / 1e3) / 1e9
+        ncu_ms = None
+        try:
+            v, unit = str(nc.get("kernel_ms_under_ncu") or "").split()
+            ncu_ms = float(v) * {"ms": 1.0, "s": 1e3, "us": 1e-3}[unit]
+        except Exception:
+            ncu_ms = None
+        if dram is not None and ncu_ms:
+            dgbs = dram / (ncu_ms / 1e3) / 1e9
             dfrac = dgbs / peak
             r["dram_gbs"] = dgbs
             r["dram_frac"] = dfrac
             r["dram_frac_nominal_8tbs"] = dgbs / NOMINAL_HBM_GBS
+            if dom["ms"] > 0:
+                r["dram_gbs_live"] = dram / (dom["ms"] / 1e3) / 1e9
+        try:
+            ifrac = float(str(nc.get("issue_active_pct")).split()[0]) / 100.0
+        except Exception:
+            ifrac = None
         inst = nc.get("warp_inst_per_launch")
-        if inst and dom["ms"] > 0 and sm_clock_mhz:
-            # issue roofline: one warp instruction per SMSP per cycle, 4 SMSPs per SM
-            ipeak = 4.0 * sms * sm_clock_mhz * 1e6
-            ach = inst / (dom["ms"] / 1e3)
-            ifrac = ach / ipeak
-            r["issue"] = {"achieved": ach, "peak": ipeak, "unit": "warp-inst/s", "frac": ifrac,
-                          "peak_basis": f"4 SMSP x {sms} SMs x {sm_clock_mhz:.0f} MHz (measured clock)",
-                          "inst_per_logical_elem": inst / max(1.0, dom["alg_bytes"] / 4.0)}
+        if ifrac is not None:
+            r["issue"] = {"active_frac": ifrac, "basis": "ncu smsp__issue_active (one warp instruction per "
+                          "SMSP per cycle is the issue peak)"}
+            if inst and ncu_ms and sm_clock_mhz:
+                r["issue"]["warp_inst_per_launch"] = inst
+                r["issue"]["inst_per_logical_elem"] = inst / max(1.0, dom["alg_bytes"] / 4.0)
         if dfrac is not None and ifrac is not None:
             r["bound"] = "hbm" if dfrac >= ifrac else "alu"
             top = nc.get("top_stall") or ""
             if max(dfrac, ifrac) < 0.6 and "long_scoreboard" in top:
-                r["limiter"] = (f"memory latency (top stall {top}; issue {ifrac:.2f}, DRAM {dfrac:.2f} of peak)")
+                r["limiter"] = (f"memory latency (top stall {top}; issue active {ifrac:.2f}, "
+                                f"DRAM {dfrac:.2f} of peak)")
             else:
                 r["limiter"] = ("HBM bandwidth" if r["bound"] == "hbm" else "instruction issue") + \
-                               f" (issue {ifrac:.2f}, DRAM {dfrac:.2f} of peak)"
+                               f" (issue active {ifrac:.2f}, DRAM {dfrac:.2f} of peak)"
     return r
 
 

@@ -106,6 +106,14 @@ constexpr uint32_t kDenseRowMul = PGABB_DENSE_ROW_MUL;
 #endif
 constexpr uint32_t kDenseRowMulWide = PGABB_DENSE_ROW_MUL_WIDE;   // for parts wider than kDenseRowWideW words
 constexpr uint32_t kDenseRowWideW = PGABB_DENSE_ROW_WIDE_W;
+#ifndef PGABB_LIST_UNROLL
+#define PGABB_LIST_UNROLL 1   // A/B: 2 loads in flight per lane lose (c2 heavy 1.72 -> 1.91 ms, c5 0.963 -> 0.996 s), 4 lose more
+#endif
+constexpr int kListUnroll = PGABB_LIST_UNROLL;
+#ifndef PGABB_CARRY_CUR
+#define PGABB_CARRY_CUR 1
+#endif
+constexpr bool kCarryCur = PGABB_CARRY_CUR;   // list index carried across rounds (no per-round ballot)   // 16-byte list loads in flight per lane (flattened lists)
 #ifndef PGABB_ROW_CHUNK
 #define PGABB_ROW_CHUNK 4
 #endif
@@ -129,7 +137,15 @@ __device__ __forceinline__ unsigned long long claim_items(unsigned long long* ne
 #endif
 constexpr int kRowMinBlocks = PGABB_ROW_MINB;   // CTAs per SM (5 x 8 warps x 4.4 KB of sets; 48 registers)
 constexpr uint32_t kSetWords = kWarpBitmapBits / 32;   // 1024 words = 4 KB per warp
-constexpr uint32_t kScratchWords = 96;                   // per-warp list descriptors
+// Batched small rows (k_tc_rows, VM = 0): heavy rows without a dense A_jx copy,
+// with |A_ix[u]| <= kBatchLa and <= 32 neighbours, are intersected several at a
+// time by one warp (batch_rows).  0 disables.
+#ifndef PGABB_BATCH_LA
+#define PGABB_BATCH_LA 0   // A/B (32): c3 p=4 26.5 -> 15.9 ms, but p=1 16.2 -> 17.3, c2 2.46 -> 8.7, c5 1.01 -> 1.17 s
+#endif
+constexpr uint32_t kBatchLa = PGABB_BATCH_LA;
+static_assert(kBatchLa <= 32, "a batch row's held list is loaded by one round of lanes");
+constexpr uint32_t kScratchWords = kBatchLa ? 128 : 96;   // per-warp list descriptors (+ batch regions)
 // per-vertex kernel: + the batch's v ids (32), the row's prefix popcounts of S
 // (1024 u16) and its hit counters (1024 u16), see VCnt
 #ifndef PGABB_VTX_SLOTS
@@ -145,7 +161,7 @@ constexpr uint32_t kVtxSlots = PGABB_VTX_SLOTS;        // u16 hit counters per w
 constexpr bool kHashFilter = PGABB_HASH_FILTER;
 constexpr uint32_t kPreGroup = PGABB_VTX_PRE_GROUP;    // S words per stored prefix popcount
 constexpr uint32_t kPreWords = (kSetWords / kPreGroup + 1) / 2;
-constexpr uint32_t kScratchWordsV = 128 + kPreWords + kVtxSlots / 2;
+constexpr uint32_t kScratchWordsV = 160 + kPreWords + kVtxSlots / 2;
 // VM (per-vertex roles, NEXT-1): 0 count only; 1 the row's lowest vertex u; 2 + the
 // middle vertex v (per pair); 3 + the highest vertex w (per hit, warp counters)
 // PGABB_VTX_INSET: the per-vertex counters of a bitmap row live in the unused
@@ -157,7 +173,7 @@ constexpr uint32_t kScratchWordsV = 128 + kPreWords + kVtxSlots / 2;
 #endif
 constexpr bool kVtxInset = PGABB_VTX_INSET;
 __host__ __device__ constexpr uint32_t scratch_words(int vm) {
-    return vm >= 3 && !kVtxInset ? kScratchWordsV : vm >= 1 ? 128u : kScratchWords;
+    return vm >= 3 && !kVtxInset ? kScratchWordsV : vm >= 1 ? 160u : kScratchWords;
 }
 
 // Per-vertex counts, third vertex w (NEXT-1): a hub w is hit by many v of the same
@@ -316,6 +332,7 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
         if (and_mask) {
             __syncwarp();
             if (use_and) scratch[32 + __popc(and_mask & lt_mask)] = v;
+            if (VM >= 1) scratch[128 + lane] = 0u;   // per-pair counts (the group's lanes add into one)
             __syncwarp();
             const uint32_t na = __popc(and_mask);
             // kAndUnroll v's per group per step: their row words are loaded before
@@ -359,8 +376,14 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                         }
                     }
                     acc += cv;
-                    if (VM >= 1 && tvj && cv) atomicAdd(tvj + vq, (unsigned long long)cv);
+                    if (VM >= 1 && tvj && cv) atomicAdd(&scratch[128 + q + z * G + g], cv);
                 }
+            }
+            if (VM >= 1 && tvj) {   // one global atomic per pair, not one per lane of its group
+                __syncwarp();
+                if ((uint32_t)lane < na && scratch[128 + lane])
+                    atomicAdd(tvj + scratch[32 + lane], (unsigned long long)scratch[128 + lane]);
+                __syncwarp();
             }
             if (use_and) lb = 0;
             PROF_MARK(3);
@@ -419,19 +442,30 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             scratch[sidx] = (lo >> 2) - excl;
             scratch[32 + sidx] = lo;
             scratch[64 + sidx] = hi;
-            if (VM >= 1) scratch[96 + sidx] = v;
+            if (VM >= 1) {
+                scratch[96 + sidx] = v;
+                scratch[128 + sidx] = 0u;   // the pair's count c_uv, summed over the rounds
+            }
         }
         __syncwarp();
-        for (uint32_t base = 0; base < total; base += 64) {
-            uint32_t vpos[2], wlo[2], whi[2], vv[2];
-            uint4 x[2];
+        // cur = (number of lists starting before the round) - 1, carried from round to
+        // round: a list starting at position rb + i (0 <= i < 32) sets bit i of starts
+        int cur = -1;
+        for (uint32_t base = 0; base < total; base += 32 * kListUnroll) {
+            uint32_t vpos[kListUnroll], wlo[kListUnroll], whi[kListUnroll], vv[kListUnroll];
+            uint4 x[kListUnroll];
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < kListUnroll; ++r) {
                 const uint32_t rb = base + 32 * r;
                 const uint32_t in = excl - rb;
-                const uint32_t bit = (lb > 0 && excl > rb && in < 32u) ? (1u << in) : 0u;
+                uint32_t bit;
+                if (kCarryCur) {
+                    bit = (lb > 0 && excl >= rb && in < 32u) ? (1u << in) : 0u;
+                } else {
+                    bit = (lb > 0 && excl > rb && in < 32u) ? (1u << in) : 0u;
+                    cur = __popc(__ballot_sync(0xffffffffu, lb > 0 && excl <= rb)) - 1;
+                }
                 const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-                const int cur = __popc(__ballot_sync(0xffffffffu, lb > 0 && excl <= rb)) - 1;
                 const uint32_t pos = rb + lane;
                 wlo[r] = 1u;
                 whi[r] = 0u;
@@ -443,16 +477,27 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
                     vpos[r] = pos + scratch[seg];
                     wlo[r] = scratch[32 + seg];
                     whi[r] = scratch[64 + seg];
-                    if (VM >= 1) vv[r] = scratch[96 + seg];
+                    if (VM >= 1) vv[r] = seg;
                     x[r] = __ldg(V + vpos[r]);
                 }
+                if (kCarryCur) cur += __popc(starts);
             }
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < kListUnroll; ++r) {
                 const int w0 = 4 * (int)vpos[r];
                 const uint32_t c = probe4<MODE, (VM >= 3)>(S, x[r], (int)wlo[r] - w0, (int)whi[r] - w0, hbits, hmask, vc);
                 acc += c;
-                if (VM >= 1 && tvj && c) atomicAdd(tvj + vv[r], (unsigned long long)c);
+                // per-pair count in shared memory: one global atomic per pair (below)
+                // instead of one per 16-byte position -- a hub v is the middle vertex
+                // of millions of triangles, and same-address global atomics serialize
+                if (VM >= 1 && tvj && c) atomicAdd(&scratch[128 + vv[r]], c);
+            }
+        }
+        if (VM >= 1 && tvj) {
+            __syncwarp();
+            if (lane < __popc(nonempty)) {
+                const uint32_t c = scratch[128 + lane];
+                if (c) atomicAdd(tvj + scratch[96 + lane], (unsigned long long)c);
             }
         }
         PROF_MARK(6);
@@ -530,6 +575,220 @@ __device__ __forceinline__ uint32_t probe_dense_row(const uint32_t* __restrict__
         if (VM >= 1 && tvj && cv) atomicAdd(tvj + v, (unsigned long long)cv);
     }
     return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Batched small rows (VM = 0): the 32 items a warp claims are loaded one per
+// lane; the rows whose streamed block has no dense copy, |A_ix[u]| <= kBatchLa
+// and <= 32 neighbours ("small") are intersected in batches of consecutive
+// small rows of one task with <= 32 neighbours in total, so the warp's lanes
+// carry up to 32 pairs (u, v) of several rows at once instead of one row's few
+// (an ER row at p = 1 has ~16): per batch one hash region per row in the warp's
+// set S (2^hb >= 2|A_ix[u]| slots, open addressing, slots hold w + 1), one lane
+// per pair loads v and its list bounds, skewed pairs binary-search the row's
+// held ids in v's list, and the rest are one flattened sequence of 16-byte
+// covers probed against their row's region (as intersect_row).  Same exact
+// |A_ix[u] ∩ A_jx[v]| sums (Listing 5).  Returns the mask of
+// lanes whose (valid) item is not small: the caller runs those one at a time.
+__device__ __forceinline__ uint32_t region_probe(const uint32_t* S, uint32_t w, uint32_t desc) {
+    const uint32_t ro = desc & 0xfffu, hb = (desc >> 12) & 15u, hm = (1u << hb) - 1u;
+    uint32_t h = hash_slot(w, hb), s;
+    while ((s = S[ro + h]) != 0u && s != w + 1) h = (h + 1) & hm;
+    return s == w + 1;
+}
+
+__device__ __forceinline__ uint32_t batch_rows(unsigned long long my_it, bool valid,
+                                               const TaskDev* __restrict__ tasks,
+                                               const uint32_t* __restrict__ col,
+                                               const uint32_t* __restrict__ rowptr, uint32_t* S,
+                                               uint32_t* scratch, int lane, uint32_t& cur_t,
+                                               unsigned long long& acc_t,
+                                               unsigned long long* __restrict__ task_counts) {
+    const uint32_t FULL = 0xffffffffu;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t le_mask = 0xffffffffu >> (31 - lane);
+    const uint32_t t = (uint32_t)(my_it >> 48), chunk = (uint32_t)(my_it >> 32) & 0xffffu, u = (uint32_t)my_it;
+    bool small = false;
+    uint32_t la = 0, ne = 0, a0 = 0, e0 = 0;
+    if (valid && chunk == 0) {
+        const TaskDev& T = tasks[t];
+        if (T.t_bm == ~0ull) {
+            a0 = __ldg(rowptr + T.s_rp + u);
+            la = __ldg(rowptr + T.s_rp + u + 1) - a0;
+            e0 = __ldg(rowptr + T.n_rp + u);
+            ne = __ldg(rowptr + T.n_rp + u + 1) - e0;
+            small = la > 0 && ne > 0 && la <= kBatchLa && ne <= 32u;
+        }
+    }
+    const uint32_t smask = __ballot_sync(FULL, small);
+    const uint32_t rest = __ballot_sync(FULL, valid) & ~smask;
+    uint32_t todo = smask;
+    while (todo) {
+        // the batch: the next small rows of the first one's task while the pairs fit
+        // the lanes and the regions the set
+        const int r0 = __ffs(todo) - 1;
+        const uint32_t t0 = __shfl_sync(FULL, t, r0);
+        const bool cand = ((todo >> lane) & 1u) && t == t0;
+        uint32_t hb = 2;
+        while ((1u << hb) < 2 * la) ++hb;
+        const uint32_t hs = cand ? (1u << hb) : 0u;
+        uint32_t incl = cand ? (ne | hs << 16) : 0u;   // ne <= 32, hs <= 64: 16-bit halves do not overflow
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t incl_ne = incl & 0xffffu, incl_hs = incl >> 16;
+        const bool inb = cand && incl_ne <= 32u && incl_hs <= kSetWords;
+        const uint32_t B = __ballot_sync(FULL, inb);
+        todo &= ~B;
+        const int rl = 31 - __clz(B);
+        const uint32_t P = __shfl_sync(FULL, incl_ne, rl);      // pairs in the batch (<= 32)
+        const uint32_t HS = __shfl_sync(FULL, incl_hs, rl);     // set words in use
+        const TaskDev& T = tasks[t0];
+        const uint32_t* __restrict__ A0 = col + T.s_col;
+        // rows by ordinal o (lane order within B): held start, region desc, la prefix
+        uint32_t incl_la = inb ? la : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl_la, o);
+            if (lane >= o) incl_la += y;
+        }
+        const uint32_t LA = __shfl_sync(FULL, incl_la, rl);
+        const uint32_t excl_la = incl_la - (inb ? la : 0u);
+        const uint32_t ord = __popc(B & lt_mask);
+        const uint32_t desc = (incl_hs - hs) | hb << 12 | la << 16;
+        __syncwarp();
+        if (inb) {
+            scratch[ord] = a0;
+            scratch[32 + ord] = desc;
+            scratch[64 + ord] = excl_la;
+        }
+        __syncwarp();
+        // stage: the held ids of all rows, flattened over the lanes
+        for (uint32_t rb = 0; rb < LA; rb += 32) {
+            const uint32_t in = excl_la - rb;
+            const uint32_t bit = (inb && excl_la >= rb && in < 32u) ? (1u << in) : 0u;
+            const uint32_t starts = __reduce_or_sync(FULL, bit);
+            const int cur = __popc(__ballot_sync(FULL, inb && excl_la < rb)) - 1;
+            const uint32_t q = rb + lane;
+            if (q < LA) {
+                const uint32_t o = cur + __popc(starts & le_mask);
+                const uint32_t d = scratch[32 + o];
+                const uint32_t w = __ldg(A0 + scratch[o] + (q - scratch[64 + o]));
+                const uint32_t ro = d & 0xfffu, hbo = (d >> 12) & 15u, hm = (1u << hbo) - 1u;
+                uint32_t h = hash_slot(w, hbo);
+                while (atomicCAS(&S[ro + h], 0u, w + 1) != 0u) h = (h + 1) & hm;
+            }
+        }
+        __syncwarp();
+        if (inb) scratch[64 + ord] = e0 - (incl_ne - ne);   // pair l of this row: neighbour e = this + l
+        __syncwarp();
+        // one lane per pair: v, its list bounds, its row's region
+        const uint32_t ebit = (inb) ? (1u << (incl_ne - ne)) : 0u;
+        const uint32_t pstarts = __reduce_or_sync(FULL, ebit);
+        uint32_t v = 0, b0 = 0, lb = 0, pd = 0, pa0 = 0;
+        if ((uint32_t)lane < P) {
+            const uint32_t o = __popc(pstarts & le_mask) - 1;
+            pa0 = scratch[o];
+            pd = scratch[32 + o];
+            const uint32_t e = scratch[64 + o] + lane;
+            v = __ldg(col + T.n_col + e);
+            const uint32_t bend = __ldg(rowptr + T.t_rp + v + 1);
+            b0 = T.n_pos != ~0ull ? __ldg(col + T.n_pos + e) + 1 : __ldg(rowptr + T.t_rp + v);
+            lb = bend - b0;
+        }
+        const uint32_t* __restrict__ Bc = col + T.t_col;
+        uint32_t acc = 0;
+        // skewed pairs: the row's held ids binary-searched in v's list (ascending, so
+        // the window only shrinks)
+        const uint32_t pla = pd >> 16;
+        if (lb > 0 && pla * log2ceil(lb + 1) * 6u < lb) {
+            uint32_t lo = 0;
+            for (uint32_t k = 0; k < pla; ++k) {
+                const uint32_t ak = __ldg(A0 + pa0 + k);
+                uint32_t hi = lb;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (__ldg(Bc + b0 + mid) < ak) lo = mid + 1; else hi = mid;
+                }
+                acc += (lo < lb && __ldg(Bc + b0 + lo) == ak);
+            }
+            lb = 0;
+        }
+        // list pairs: flattened 16-byte covers (see intersect_row), each probed
+        // against its own row's region
+        const uint32_t nonempty = __ballot_sync(FULL, lb > 0);
+        if (nonempty) {
+            const uint4* __restrict__ V = reinterpret_cast<const uint4*>((uintptr_t)Bc & ~uintptr_t(15));
+            const uint32_t coff = (uint32_t)(((uintptr_t)Bc & 15) >> 2);
+            const uint32_t lo = coff + b0, hi = lo + lb;
+            const uint32_t nv = lb ? ((hi + 3) >> 2) - (lo >> 2) : 0u;
+            uint32_t vin = nv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, vin, o);
+                if (lane >= o) vin += y;
+            }
+            const uint32_t total = __shfl_sync(FULL, vin, 31);
+            const uint32_t excl = vin - nv;
+            __syncwarp();
+            if (lb > 0) {
+                const uint32_t sidx = __popc(nonempty & lt_mask);
+                scratch[sidx] = (lo >> 2) - excl;
+                scratch[32 + sidx] = lo;
+                scratch[64 + sidx] = hi;
+                scratch[96 + sidx] = pd;
+            }
+            __syncwarp();
+            for (uint32_t base = 0; base < total; base += 64) {
+                uint32_t vpos[2], wlo[2], whi[2], dd[2];
+                uint4 x[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t rb = base + 32 * r;
+                    const uint32_t in = excl - rb;
+                    const uint32_t bit = (lb > 0 && excl > rb && in < 32u) ? (1u << in) : 0u;
+                    const uint32_t starts = __reduce_or_sync(FULL, bit);
+                    const int cur = __popc(__ballot_sync(FULL, lb > 0 && excl <= rb)) - 1;
+                    const uint32_t pos = rb + lane;
+                    wlo[r] = 1u;
+                    whi[r] = 0u;
+                    x[r] = make_uint4(0, 0, 0, 0);
+                    vpos[r] = 0;
+                    dd[r] = 0;
+                    if (pos < total) {
+                        const uint32_t seg = cur + __popc(starts & le_mask);
+                        vpos[r] = pos + scratch[seg];
+                        wlo[r] = scratch[32 + seg];
+                        whi[r] = scratch[64 + seg];
+                        dd[r] = scratch[96 + seg];
+                        x[r] = __ldg(V + vpos[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int w0 = 4 * (int)vpos[r];
+                    const int l0 = (int)wlo[r] - w0, h0 = (int)whi[r] - w0;
+                    if (l0 <= 0 && 0 < h0) acc += region_probe(S, x[r].x, dd[r]);
+                    if (l0 <= 1 && 1 < h0) acc += region_probe(S, x[r].y, dd[r]);
+                    if (l0 <= 2 && 2 < h0) acc += region_probe(S, x[r].z, dd[r]);
+                    if (l0 <= 3 && 3 < h0) acc += region_probe(S, x[r].w, dd[r]);
+                }
+            }
+        }
+        __syncwarp();
+        for (uint32_t k = lane; k < HS; k += 32) S[k] = 0u;   // the set is all-zero between rows
+        __syncwarp();
+        const uint32_t sum = __reduce_add_sync(FULL, acc);
+        if (t0 != cur_t) {
+            if (lane == 0 && acc_t) atomicAdd(&task_counts[cur_t], acc_t);
+            cur_t = t0;
+            acc_t = 0;
+        }
+        acc_t += sum;
+    }
+    return rest;
 }
 
 constexpr int kLightThreads = 256;
@@ -640,7 +899,7 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     const int wid = threadIdx.x >> 5;
     uint32_t* S = smem + wid * (kSetWords + scratch_words(VM));
     uint32_t* scratch = S + kSetWords;
-    uint32_t* vpre = scratch + 128;                  // VTX only (see VCnt; per row when inset)
+    uint32_t* vpre = scratch + 160;                  // VTX only (see VCnt; per row when inset)
     uint32_t* vcnt = vpre + kPreWords;
     for (uint32_t k = lane; k < kSetWords; k += 32) S[k] = 0;   // invariant: all-zero between rows
     if (VM >= 3 && !kVtxInset)
@@ -649,8 +908,12 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     // Warps claim kRowChunk items at a time from one counter, so the items in
     // flight stay a narrow window of the locality-ordered list (the A_jx blocks
     // they share stay in L2).
-    unsigned long long claim_end = 0;
-    unsigned long long idx = claim_items(next, nitems, lane, claim_end);
+    // counting kernel: 32 items per claim, small rows batched (batch_rows); the
+    // other rows, one at a time below
+    constexpr bool kBat = VM == 0 && !TIMED && kBatchLa > 0;
+    unsigned long long claim_end = 0, idx = 0, my_it = 0;
+    uint32_t pend = 0;
+    if (!kBat) idx = claim_items(next, nitems, lane, claim_end);
     uint32_t cur_t = 0;                              // task of the warp's running count
     unsigned long long acc_t = 0;
 #ifdef PGABB_PROF
@@ -659,12 +922,34 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
     unsigned long long pt = clock64();
 #endif
     for (;;) {
-        if (idx >= nitems) break;
-        const unsigned long long it = __ldg(items + idx);
+        unsigned long long it;
+        if (kBat) {
+            bool done = false;
+            while (pend == 0) {
+                unsigned long long b = 0;
+                if (lane == 0) b = atomicAdd(next, 32ull);
+                b = __shfl_sync(0xffffffffu, b, 0);
+                if (b >= nitems) {
+                    done = true;
+                    break;
+                }
+                const bool valid = b + lane < nitems;
+                my_it = valid ? __ldg(items + b + lane) : 0ull;
+                pend = batch_rows(my_it, valid, tasks, col, rowptr, S, scratch, lane, cur_t, acc_t, task_counts);
+                PROF_MARK(10);
+            }
+            if (done) break;
+            const int sl = __ffs(pend) - 1;
+            pend &= pend - 1;
+            it = __shfl_sync(0xffffffffu, my_it, sl);
+        } else {
+            if (idx >= nitems) break;
+            it = __ldg(items + idx);
+            idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
+        }
         const uint32_t t = (uint32_t)(it >> 48);
         const uint32_t chunk = (uint32_t)(it >> 32) & 0xffffu;
         const uint32_t u = (uint32_t)it;
-        idx = idx + 1 < claim_end ? idx + 1 : claim_items(next, nitems, lane, claim_end);
         const long long c0 = TIMED ? clock64() : 0;
         // kernel roles (internal.h TaskDev, DESIGN R25): u is the item's row vertex,
         // A its held list, vcol its neighbours (chunk `chunk` of them), Bc/rp_jx the

@@ -185,7 +185,10 @@ static_assert(sizeof(TaskDev) == 88, "TaskDev layout");
 // A block gets a dense bitmap copy (rows of ceil(w/32) words) when its density is
 // at least 1/kDenseInv and its column part is narrow enough for a warp bitmap:
 // then the copy is no larger than the list form.
-constexpr uint64_t kDenseInv = 32;
+#ifndef PGABB_DENSE_INV
+#define PGABB_DENSE_INV 32
+#endif
+constexpr uint64_t kDenseInv = PGABB_DENSE_INV;
 
 // A heavy row item: (task, local row r, chunk c) with the row's held list and
 // neighbour list non-empty; the warp takes neighbours [c*kChunkNbrs, (c+1)*kChunkNbrs)

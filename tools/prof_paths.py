@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 CATS = {0: "item setup", 1: "probe_dense_row", 2: "stage set", 3: "dense AND", 4: "skew search",
         5: "long lists", 6: "short flattened", 7: "reduce+atomic", 8: "mode2 fallback",
-        9: "batch header", 16: "#items dense-row", 17: "#items bitmap", 18: "#items hash",
+        9: "batch header", 10: "batched small rows", 16: "#items dense-row", 17: "#items bitmap", 18: "#items hash",
         19: "#items mode2"}
 
 
@@ -42,15 +42,15 @@ def run(names):
         cfg = CONFIGS[name]
         n, s, d = cfg.generate()
         with pg.build_blocks(n, s, d, p=cfg.p) as b:
-            run1 = (lambda: int(b.vertex_triangles().sum()) // 3) if path == "vertex" else b.triangle_count
+            run1 = (lambda: int(b.vertex_triangles()[0].sum()) // 3) if path == "vertex" else b.triangle_count
             run1()
             lib.pgabb_prof_read(buf, 1)
             T = run1()
             ms = b.stats()["ms_main_kernel_last"]
             lib.pgabb_prof_read(buf, 1)
-        tot = sum(buf[c] for c in range(10))
+        tot = sum(buf[c] for c in range(11))
         res = {"config": spec, "triangles": T, "kernel_ms": ms,
-               "share": {CATS[c]: round(buf[c] / max(tot, 1), 4) for c in range(10)},
+               "share": {CATS[c]: round(buf[c] / max(tot, 1), 4) for c in range(11)},
                "counts": {CATS[c]: int(buf[c]) for c in range(16, 20)}}
         print(json.dumps(res), flush=True)
 
