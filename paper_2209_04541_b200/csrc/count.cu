@@ -168,6 +168,14 @@ constexpr uint32_t kScratchWordsV = 160 + kPreWords + kVtxSlots / 2;
 // tail of the warp's 4 KB set (a part of W <= kInsetMaxW words leaves 1024 - W
 // words free), so the VM = 3 kernel keeps the counting kernel's footprint and
 // occupancy; hash-set rows then credit w with global atomics.
+#ifndef PGABB_VTX_SLICED
+#define PGABB_VTX_SLICED 1
+#endif
+constexpr bool kVtxSliced = PGABB_VTX_SLICED;   // per-vertex dense pairs: bit-sliced hit counters (and_vtx)
+#ifndef PGABB_VTX_MATCH
+#define PGABB_VTX_MATCH 1
+#endif
+constexpr bool kVtxMatch = PGABB_VTX_MATCH;     // per-vertex list hits: warp-aggregated by w (probe4)
 #ifndef PGABB_VTX_INSET
 #define PGABB_VTX_INSET 1
 #endif
@@ -270,9 +278,39 @@ __device__ __forceinline__ uint32_t probe1(const uint32_t* S, uint32_t w, uint32
     return h;
 }
 
+// n hits on w (a member of S), credited at once (warp-aggregated hits)
+template <int MODE>
+__device__ __forceinline__ void vhit_n(const VCnt& vc, const uint32_t* S, uint32_t w, uint32_t hbits, uint32_t hmask,
+                                       uint32_t n) {
+    if (!vc.on) {
+        atomicAdd(vc.tvx + w, (unsigned long long)n);
+        return;
+    }
+    const uint32_t idx = MODE == 0 ? rank_in_set(S, vc.pre, w) : hash_find(S, w, hbits, hmask);
+    atomicAdd(&vc.cnt[idx >> 1], n << ((idx & 1u) << 4));
+}
+
 template <int MODE, bool VTX>
 __device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int lo, int hi, uint32_t hbits,
                                            uint32_t hmask, const VCnt& vc) {
+    if (VTX && kVtxMatch) {
+        // per-vertex kernel: the lanes hitting the same w in one component (a hub w
+        // sits in many of the round's lists) add once, with their count -- the
+        // shared counters would otherwise serialise the conflicting atomics
+        const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t h = (lo <= j && j < hi) ? probe<MODE>(S, ws[j], hbits, hmask) : 0u;
+            c += h;
+            const uint32_t hb = __ballot_sync(0xffffffffu, h);
+            if (h) {
+                const uint32_t m = __match_any_sync(hb, ws[j]);
+                if ((threadIdx.x & 31) == __ffs(m) - 1) vhit_n<MODE>(vc, S, ws[j], hbits, hmask, __popc(m));
+            }
+        }
+        return c;
+    }
     if (lo <= 0 && hi >= 4)
         return probe1<MODE, VTX>(S, x.x, hbits, hmask, vc) + probe1<MODE, VTX>(S, x.y, hbits, hmask, vc) +
                probe1<MODE, VTX>(S, x.z, hbits, hmask, vc) + probe1<MODE, VTX>(S, x.w, hbits, hmask, vc);
@@ -285,6 +323,65 @@ __device__ __forceinline__ uint32_t probe4(const uint32_t* S, const uint4 x, int
 }
 
 __device__ __forceinline__ uint32_t log2ceil(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+// Dense pairs of the per-vertex kernel (VM >= 3): every hit w must be credited,
+// and hits concentrate on a few hub words, so instead of a per-bit loop per lane
+// (a lane holding a hub word serialises the warp) each lane counts its word's
+// hits over the batch's v's in six bit-sliced counters c0..c5 (bit b of c_j =
+// bit j of w = 32k + b's count; <= 32 v's per batch) with a ripple-carry add
+// per v, and credits each w once per batch with its count.  Lane (g, kl) takes
+// words kl, kl + gsz, ... and the v's g, g + G, ... (G groups of gsz lanes, as
+// the counting path).  pairs: each v's c_uv is also summed into scratch[128 + q].
+__device__ __forceinline__ uint32_t and_vtx(const uint32_t* S, const uint32_t* __restrict__ BM, uint32_t W,
+                                            uint32_t na, uint32_t* scratch, uint32_t gsz, uint32_t G, uint32_t g,
+                                            uint32_t kl, const VCnt& vc, bool pairs) {
+    const uint32_t FULL = 0xffffffffu;
+    uint32_t acc = 0;
+    for (uint32_t k0 = 0; k0 < W; k0 += gsz) {
+        const uint32_t k = k0 + kl;
+        const uint32_t s = k < W ? S[k] : 0u;
+        if (!__any_sync(FULL, s)) continue;
+        uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+        const uint32_t nq = (na + G - 1) / G;
+#pragma unroll 4
+        for (uint32_t i = 0; i < nq; ++i) {
+            const uint32_t q = g + G * i;
+            uint32_t x = 0;
+            if (q < na && s) x = s & __ldg(BM + (uint64_t)scratch[32 + q] * W + k);
+            const uint32_t px = __popc(x);
+            acc += px;
+            if (pairs) {
+                uint32_t pc = px;
+                if (G == 1) {
+                    pc = __reduce_add_sync(FULL, pc);
+                } else {
+                    for (uint32_t o = gsz >> 1; o; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+                }
+                if (kl == 0 && q < na && pc) scratch[128 + q] += pc;
+            }
+            uint32_t cy = x, t;
+            t = c0 & cy; c0 ^= cy; cy = t;
+            t = c1 & cy; c1 ^= cy; cy = t;
+            t = c2 & cy; c2 ^= cy; cy = t;
+            t = c3 & cy; c3 ^= cy; cy = t;
+            t = c4 & cy; c4 ^= cy; cy = t;
+            c5 ^= cy;
+        }
+        for (uint32_t nz = c0 | c1 | c2 | c3 | c4 | c5; nz; nz &= nz - 1u) {
+            const uint32_t b = __ffs(nz) - 1;
+            const uint32_t cnt = ((c0 >> b) & 1u) | ((c1 >> b) & 1u) << 1 | ((c2 >> b) & 1u) << 2 |
+                                 ((c3 >> b) & 1u) << 3 | ((c4 >> b) & 1u) << 4 | ((c5 >> b) & 1u) << 5;
+            const uint32_t w = 32u * k + b;
+            if (vc.on) {
+                const uint32_t idx = rank_in_set(S, vc.pre, w);
+                atomicAdd(&vc.cnt[idx >> 1], cnt << ((idx & 1u) << 4));
+            } else {
+                atomicAdd(vc.tvx + w, (unsigned long long)cnt);
+            }
+        }
+    }
+    return acc;
+}
 
 // VM (per-vertex roles, NEXT-1): VM >= 2 adds each pair's count c_uv to tvj[v],
 // VM >= 3 counts each common element w for w (warp counters, VCnt); the row
@@ -338,6 +435,8 @@ __device__ __forceinline__ uint32_t intersect_row(const uint32_t* __restrict__ v
             // kAndUnroll v's per group per step: their row words are loaded before
             // any is used, so that many loads are in flight per lane
             constexpr int U = R > 0 ? kAndUnroll : 1;
+            if (VM >= 3 && kVtxSliced) acc += and_vtx(S, BM, W, na, scratch, gsz, G, g, kl, vc, tvj != nullptr);
+            else
             for (uint32_t q = 0; q < na; q += U * G) {
                 uint32_t vqs[U], wds[U][R > 0 ? R : 1];
 #pragma unroll
@@ -888,8 +987,12 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
 // TIMED (pgabb_task_times only): lane 0 adds each item's clock64 span to cyc[t].
 #define IROW(M, R_, ...) \
     (npos ? intersect_row<M, R_, VM, true>(__VA_ARGS__) : intersect_row<M, R_, VM, false>(__VA_ARGS__))
+#ifndef PGABB_ROW_MINB_VTX
+#define PGABB_ROW_MINB_VTX 4
+#endif
+constexpr int kRowMinBlocksVtx = PGABB_ROW_MINB_VTX;   // the VM = 3 kernel: 64 registers (bit-sliced counters)
 template <int VM, bool TIMED>
-__global__ void __launch_bounds__(kRowWarps * 32, kRowMinBlocks)
+__global__ void __launch_bounds__(kRowWarps * 32, VM >= 3 ? kRowMinBlocksVtx : kRowMinBlocks)
 k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitems, const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
           const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
           unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
