@@ -44,6 +44,8 @@ def parse(argv=None):
     ap.add_argument("--cut-rule", type=int, default=0)
     ap.add_argument("--orient", default="auto", choices=["auto", "low", "mid"],
                     help="task orientation (DESIGN R25): per task the one streaming fewer ids, or all LOW / MID")
+    ap.add_argument("--light-held", type=int, default=0, choices=[0, 8, 15],
+                    help="thread-per-row items up to 8 or 15 held ids (DESIGN R29); 0 = auto")
     ap.add_argument("--path", choices=["count", "vertex", "vertex2", "cc"], default="count",
                     # vertex2: the two-pass route of R24 (measured far slower: kept for the record)
                     help="count: T (the headline); vertex: per-vertex t(v) (SURVEY 8(f) NEXT-1); "
@@ -426,12 +428,12 @@ def run_ours(args):
     if ws > 1 and args.balance == "measured":
         # S8 with rank 0's measured task times broadcast to all ranks (DESIGN R22; untimed)
         from paper_2209_04541_b200 import dist as pgd
-        b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient)
+        b = pgd.build_blocks_balanced(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held)
     elif args.budget_gb > 0:
-        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held, device=dev, rank=rank, world_size=ws,
                             residency=pg.RESIDENT_HOST, device_budget_bytes=int(args.budget_gb * (1 << 30)))
     else:
-        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws)
+        b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held, device=dev, rank=rank, world_size=ws)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
     # a real (non-legacy-default) stream: the library orders its work on it and the
@@ -444,7 +446,7 @@ def run_ours(args):
     tv_dev = torch.zeros(max(n, 1), dtype=torch.int64, device="cuda") if vertex else None
     b_rev = None
     if args.path == "vertex2":   # the reversed-order handle of the two-pass route (R24)
-        b_rev = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
+        b_rev = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held, device=dev, rank=rank, world_size=ws,
                                 reverse_order=True)
 
     def step():
@@ -522,12 +524,13 @@ def run_ours(args):
     roofline = roofline_of(args.config, kernels, ms_per_step, peak, peak_src, vertex,
                            clocks.get("sm_mhz") or 1965.0, torch.cuda.get_device_properties(dev).multi_processor_count)
     roofline["s10_combined"] = kern("k_tc_rows + k_tc_light", kms, alg)
-    roofline["items"] = {"heavy": int(st["items_heavy"]), "light": int(st["items_light"])}
+    roofline["items"] = {"heavy": int(st["items_heavy"]), "light": int(st["items_light"]),
+                         "medium": int(st["items_medium"]), "light_held": int(st["light_held"])}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
     if not args.no_e2e and not vertex and args.budget_gb <= 0:
-        bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=dev, rank=rank, world_size=ws,
+        bh = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held, device=dev, rank=rank, world_size=ws,
                              residency=pg.RESIDENT_HOST, host_permille=args.host_permille,
                              task_weights=getattr(b, "task_weights_used", None))
         for _ in range(max(1, args.warmup)):
@@ -619,7 +622,7 @@ def run_cc(args):
     cfg = CONFIGS[args.config]
     p = args.p or cfg.p
     n, s, d = cfg.generate()
-    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, device=0)
+    b = pg.build_blocks(n, s, d, p=p, cut_rule=args.cut_rule, orient=args.orient, light_held=args.light_held, device=0)
     st0 = b.stats()
     m_edges = int(st0["m_edges"])
     lab = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")

@@ -34,7 +34,7 @@ class Config:
 CONFIGS = {
     "c1": Config("c1", "R-MAT scale 10, edge factor 16, 2x2 blocks", 2, "rmat", (10, 16, 1)),
     "c2": Config("c2", "R-MAT scale 20, edge factor 16, 8x8 blocks", 8, "rmat", (20, 16, 1)),
-    "c3": Config("c3", "Erdos-Renyi n=2^24, avg degree 32, 16x16 blocks", 16, "er", (1 << 24, 32, 1)),
+    "c3": Config("c3", "Erdos-Renyi n=2^24, avg degree 32, 4x4 blocks", 4, "er", (1 << 24, 32, 1)),
     # p = 1: measured on B200 (round 2: count 1.09 / 1.45 / 1.65 / 1.84 / 2.09 ms at
     # p = 1 / 2 / 3 / 4 / 6): a low-degree grid gains nothing from narrow parts and pays
     # per (edge, part) pair

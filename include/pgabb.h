@@ -125,6 +125,11 @@ typedef struct {
                                    EINVAL with another residency, a budget, or > 1000.  Counts
                                    are unchanged; per-vertex counts and task times need 0. */
     uint32_t host_threads;      /* host threads for host_permille (0 = all hardware threads) */
+    uint32_t light_held;        /* thread-per-row items (DESIGN R20, R29): 8 = rows with <= 8
+                                   held ids; 15 = also rows with 9..15 held ids (a second
+                                   kernel instantiation with 15 registers for them; heavy
+                                   warp items otherwise); 0 = auto (DESIGN R29).  Other
+                                   values: EINVAL.  Counts are identical for every value. */
 } pgabb_build_opts_t;
 
 #define PGABB_ORIENT_AUTO 0u
@@ -248,6 +253,8 @@ typedef struct {
     double ms_cc_last;                  /* device time of the last pgabb_connected_components */
     double ms_host_last;                /* host_permille > 0: wall time of the host threads' share
                                            of the last count (runs concurrently with the GPU) */
+    uint64_t items_medium;              /* of items_light: the medium ones (9..15 held ids, R29) */
+    uint64_t light_held;                /* the build's light_held (8 or 15; auto resolved) */
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);

@@ -283,7 +283,7 @@ ORIENTS = {"auto": 0, "low": 1, "mid": 2}
 def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = -1, rank: int = 0,
                  world_size: int = 1, residency: int = RESIDENT_DEVICE, device_budget_bytes: int = 0,
                  task_weights=None, reverse_order: bool = False, orient="auto", host_permille: int = 0,
-                 host_threads: int = 0) -> Blocks:
+                 host_threads: int = 0, light_held: int = 0) -> Blocks:
     """S1..S8: canonicalise, degree-order, orient, cut, block, enumerate, cost, assign.
 
     orient: task orientation (DESIGN R25) -- "auto" (per task, fewer streamed ids),
@@ -292,6 +292,8 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     host_permille / host_threads: collaborative CPU + GPU (NEXT-3) on a host-resident
     handle -- the sparsest pieces up to this share of the cost are counted by host
     threads while the GPU counts the rest.
+    light_held: largest held list of a thread-per-row item -- 8, 15 (rows with 9..15
+    held ids get the second thread-per-row kernel) or 0 = auto (DESIGN R29).
 
     src/dst: uint32 tuples as numpy arrays (host) or torch CUDA tensors (device).
     task_weights: optional per-task estimates E(t) (e.g. Blocks.task_times() of a
@@ -310,6 +312,7 @@ def build_blocks(n: int, src, dst, p: int = 0, cut_rule: int = 0, device: int = 
     o.reverse_order = int(bool(reverse_order))
     o.orient = ORIENTS[orient] if isinstance(orient, str) else int(orient)
     o.host_permille, o.host_threads = int(host_permille), int(host_threads)
+    o.light_held = int(light_held)
     o.device_budget_bytes = device_budget_bytes
     tw = None
     if task_weights is not None:

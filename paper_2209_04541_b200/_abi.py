@@ -34,7 +34,7 @@ class BuildOpts(ctypes.Structure):
     _fields_ = [("p", u32), ("cut_rule", u32), ("device", i32), ("inputs_on_device", u32),
                 ("rank", i32), ("world_size", i32), ("residency", u32), ("reverse_order", u32),
                 ("device_budget_bytes", u64), ("task_weights", u64p), ("n_task_weights", u64),
-                ("orient", u32), ("host_permille", u32), ("host_threads", u32)]
+                ("orient", u32), ("host_permille", u32), ("host_threads", u32), ("light_held", u32)]
 
 
 class CountOpts(ctypes.Structure):
@@ -51,7 +51,7 @@ class Stats(ctypes.Structure):
                 ("alg_bytes_light", u64), ("d2d_bytes_last", u64), ("ms_build", ctypes.c_double),
                 ("ms_count_last", ctypes.c_double), ("ms_main_kernel_last", ctypes.c_double),
                 ("ms_light_kernel_last", ctypes.c_double), ("ms_cc_last", ctypes.c_double),
-                ("ms_host_last", ctypes.c_double)]
+                ("ms_host_last", ctypes.c_double), ("items_medium", u64), ("light_held", u64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}

@@ -147,6 +147,11 @@ pgabb_status_t pgabb_build_blocks(uint32_t n, uint64_t m, const uint32_t* src, c
         if (o.host_permille && (o.residency != PGABB_RESIDENT_HOST || o.device_budget_bytes))
             fail(PGABB_EINVAL, "host_permille needs PGABB_RESIDENT_HOST without a device budget");
         h->host_permille = o.host_permille;
+        if (o.light_held != 0 && o.light_held != kLightLa && o.light_held != kMedLa)
+            fail(PGABB_EINVAL, "light_held must be 0 (auto), " + std::to_string(kLightLa) + " or " +
+                                   std::to_string(kMedLa));
+        h->light_held = o.light_held ? o.light_held : kMedLa;
+        h->light_auto = o.light_held == 0;
         h->host_threads = o.host_threads;
         h->budget = o.device_budget_bytes;
         h->streaming = (h->residency == PGABB_RESIDENT_HOST && h->budget > 0);
@@ -310,6 +315,8 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->ms_host_last = b->ms_host_last;
         s->items_heavy = b->n_items;
         s->items_light = b->n_light;
+        s->items_medium = b->n_light - b->n_light0;
+        s->light_held = b->light_held;
         s->alg_bytes_light = b->alg_light;
         s->d2d_bytes_last = b->d2d_last;
     });

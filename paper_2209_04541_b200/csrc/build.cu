@@ -438,31 +438,39 @@ __device__ __forceinline__ uint32_t streamed_len(const TaskDev& T, const uint32_
     return end - beg;
 }
 
+// held_max: kLightLa, or kMedLa when medium rows (kLightLa < |S| <= kMedLa, R29) get
+// mf = 1 for the second thread-per-row kernel instead of heavy items.
 __global__ void k_row_flags(PieceDev w, const TaskDev* tasks, const uint32_t* col, const uint32_t* rowptr,
-                            uint32_t* hf, uint32_t* lf, unsigned long long* alg) {
+                            uint32_t* hf, uint32_t* lf, uint32_t* mf, uint32_t held_max, unsigned long long* alg) {
     const TaskDev T = tasks[w.task];
     const uint32_t nr = w.r1 - w.r0;
     for (uint64_t k0 = blockIdx.x * (uint64_t)blockDim.x; k0 <= nr; k0 += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = k0 + threadIdx.x;
-        uint32_t fh = 0, fl = 0;
+        uint32_t fh = 0, fl = 0, fm = 0;
         unsigned long long bytes = 0;
         if (k < nr) {
             const uint32_t r = w.r0 + (uint32_t)k;
             const uint32_t e0 = rowptr[T.n_rp + r], e1 = rowptr[T.n_rp + r + 1];
             const uint32_t la = rowptr[T.s_rp + r + 1] - rowptr[T.s_rp + r];
             if (e1 > e0 && la > 0) {
-                bool light = la <= kLightLa && e1 - e0 <= kLightLe;
+                bool light = la <= held_max && e1 - e0 <= kLightLe;
                 if (light) {
-                    uint32_t work = 0, lsum = 0;
+                    uint32_t work = 0, lsum = 0, lmax = 0;
                     for (uint32_t e = e0; e < e1; ++e) {
                         const uint32_t lb = streamed_len(T, col, rowptr, e);
                         work += light_pair_loads(la, lb);
                         lsum += lb;
+                        lmax = max(lmax, lb);
                     }
                     light = T.t_bm != ~0ull || work <= kLightWork;
+                    // a medium row only when every streamed list is a short scanned list (no
+                    // per-id binary searches, no dense block: R-MAT rows against hub lists
+                    // or bitmaps stay heavy warp items, R29)
+                    if (la > kLightLa && (T.t_bm != ~0ull || lmax > kLightScan)) light = false;
                     bytes = 4ull * (la + lsum) + 12ull * (e1 - e0);
                 }
-                fl = light;
+                fl = light && la <= kLightLa;
+                fm = light && la > kLightLa;
                 fh = light ? 0u : heavy_chunks(e1 - e0);
                 if (!light) bytes = 0;
             }
@@ -470,6 +478,7 @@ __global__ void k_row_flags(PieceDev w, const TaskDev* tasks, const uint32_t* co
         if (k <= nr) {
             hf[k] = fh;
             lf[k] = fl;
+            mf[k] = fm;
         }
         if (alg) {
             for (int o = 16; o > 0; o >>= 1) bytes += __shfl_down_sync(0xffffffffu, bytes, o);
@@ -1203,6 +1212,8 @@ void plan_waves(pgabb_blocks_s* h) {
         cur.item_end = h->piece_item_off[cur.piece_end];
         cur.light_begin = h->piece_light_off[cur.piece_begin];
         cur.light_end = h->piece_light_off[cur.piece_end];
+        cur.med_begin = h->piece_med_off[cur.piece_begin];
+        cur.med_end = h->piece_med_off[cur.piece_end];
         cur.task_table = h->waves.size();
         wtasks.insert(wtasks.end(), cur_tasks.begin(), cur_tasks.end());
         h->waves.push_back(cur);
@@ -1426,20 +1437,18 @@ void upload_work(pgabb_blocks_s* h) {
     const std::vector<size_t> order = locality_order(h);
     uint32_t maxrows = 0;
     for (const PieceDev& w : h->work) maxrows = std::max(maxrows, w.r1 - w.r0);
-    DBuf<uint32_t> hf, lf, hpos, lpos;
+    DBuf<uint32_t> hf, lf, mf, hpos, lpos, mpos;
     DBuf<unsigned char> tmp;
-    hf.alloc((size_t)maxrows + 1);
-    lf.alloc((size_t)maxrows + 1);
-    hpos.alloc((size_t)maxrows + 1);
-    lpos.alloc((size_t)maxrows + 1);
-    std::vector<uint64_t> piece_items(h->work.size(), 0), piece_light(h->work.size(), 0);
+    for (DBuf<uint32_t>* b : {&hf, &lf, &mf, &hpos, &lpos, &mpos}) b->alloc((size_t)maxrows + 1);
+    std::vector<uint64_t> piece_items(h->work.size(), 0), piece_light(h->work.size(), 0),
+        piece_med(h->work.size(), 0);
     DBuf<unsigned long long> d_alg;
     d_alg.alloc(1);
     PG_CK(cudaMemsetAsync(d_alg.p, 0, 8, st));
     auto classify = [&](const PieceDev& w, unsigned long long* alg) {
         const uint32_t nr = w.r1 - w.r0;
         k_row_flags<<<grid_for(nr + 1), kThreads, 0, st>>>(w, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, hf.p, lf.p,
-                                                           alg);
+                                                           mf.p, h->light_held, alg);
         PG_LAUNCH_CHECK();
         cub_call([&](void* tp, size_t& b) {
             return cub::DeviceScan::ExclusiveSum(tp, b, hf.p, hpos.p, (int64_t)nr + 1, st);
@@ -1447,38 +1456,64 @@ void upload_work(pgabb_blocks_s* h) {
         cub_call([&](void* tp, size_t& b) {
             return cub::DeviceScan::ExclusiveSum(tp, b, lf.p, lpos.p, (int64_t)nr + 1, st);
         }, st, tmp);
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(tp, b, mf.p, mpos.p, (int64_t)nr + 1, st);
+        }, st, tmp);
     };
     // pass 1: count per piece; item offsets per piece in locality order (the waves of
     // streaming residency are contiguous ranges of them)
     h->piece_item_off.assign(order.size() + 1, 0);
     h->piece_light_off.assign(order.size() + 1, 0);
-    for (size_t k : order) {
-        const PieceDev& w = h->work[k];
-        const uint32_t nr = w.r1 - w.r0;
-        classify(w, d_alg.p);
-        uint32_t cnt[2] = {0, 0};
-        PG_CK(cudaMemcpyAsync(&cnt[0], hpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
-        PG_CK(cudaMemcpyAsync(&cnt[1], lpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
-        PG_CK(cudaStreamSynchronize(st));
-        piece_items[k] = cnt[0];
-        piece_light[k] = cnt[1];
+    h->piece_med_off.assign(order.size() + 1, 0);
+    auto count_pass = [&]() {
+        uint64_t nh = 0, nm = 0;
+        PG_CK(cudaMemsetAsync(d_alg.p, 0, 8, st));
+        for (size_t k : order) {
+            const PieceDev& w = h->work[k];
+            const uint32_t nr = w.r1 - w.r0;
+            classify(w, d_alg.p);
+            uint32_t cnt[3] = {0, 0, 0};
+            PG_CK(cudaMemcpyAsync(&cnt[0], hpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaMemcpyAsync(&cnt[1], lpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaMemcpyAsync(&cnt[2], mpos.p + nr, 4, cudaMemcpyDeviceToHost, st));
+            PG_CK(cudaStreamSynchronize(st));
+            piece_items[k] = cnt[0];
+            piece_light[k] = cnt[1];
+            piece_med[k] = cnt[2];
+            nh += cnt[0];
+            nm += cnt[2];
+        }
+        return std::make_pair(nh, nm);
+    };
+    const auto [n_heavy1, n_med1] = count_pass();
+    // auto (R29): the medium kernel only when its rows are at least half of what would
+    // otherwise be heavy items (low-skew graphs: ER at small p); else they stay heavy
+    if (h->light_auto && h->light_held > kLightLa && 2 * n_med1 < n_heavy1 + n_med1) {
+        h->light_held = kLightLa;
+        count_pass();
     }
-    uint64_t nitems = 0, nlight = 0;
+    // the light list holds every piece's light items, then every piece's medium items
+    uint64_t nitems = 0, nlight = 0, nmed = 0;
+    for (size_t q = 0; q < order.size(); ++q) nlight += piece_light[order[q]];
     for (size_t q = 0; q < order.size(); ++q) {
         nitems += piece_items[order[q]];
-        nlight += piece_light[order[q]];
         h->piece_item_off[q + 1] = nitems;
-        h->piece_light_off[q + 1] = nlight;
+        h->piece_light_off[q + 1] = h->piece_light_off[q] + piece_light[order[q]];
+        h->piece_med_off[q] = nlight + nmed;
+        nmed += piece_med[order[q]];
     }
+    h->piece_med_off[order.size()] = nlight + nmed;
     h->n_items = nitems;
-    h->n_light = nlight;
+    h->n_light0 = nlight;
+    h->n_light = nlight + nmed;
     unsigned long long alg_light = 0;
     PG_COPY_SYNC(&alg_light, d_alg.p, 8, st);
     h->alg_light = alg_light;
     h->d_items.alloc(std::max<uint64_t>(nitems, 1));
-    h->d_light.alloc(std::max<uint64_t>(nlight, 1));
+    h->d_light.alloc(std::max<uint64_t>(h->n_light, 1));
     uint64_t max_light = 0;
     for (uint64_t c : piece_light) max_light = std::max(max_light, c);
+    for (uint64_t c : piece_med) max_light = std::max(max_light, c);
     DBuf<uint32_t> lkey, lkey2;
     DBuf<uint4> litem2;
     if (max_light) {
@@ -1487,31 +1522,34 @@ void upload_work(pgabb_blocks_s* h) {
         litem2.alloc(max_light);
     }
     // pass 2: emit in layout order
-    uint64_t base = 0, lbase = 0;
+    uint64_t base = 0, lbase = 0, mbase = nlight;
+    // a piece's light (or medium) items, then sorted by work (stable: rows ascending
+    // within equal work)
+    auto emit_light = [&](const PieceDev& w, const uint32_t* flags, const uint32_t* pos, uint4* li, int64_t nl) {
+        const uint32_t nr = w.r1 - w.r0;
+        k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_tasks.p, flags, pos, h->d_col.p, h->d_rowptr.p,
+                                                        li, lkey.p);
+        PG_LAUNCH_CHECK();
+        const int kb = 8 + bits_for((uint64_t)(nl - 1) / kLightSortWindow);
+        cub_call([&](void* tp, size_t& b) {
+            return cub::DeviceRadixSort::SortPairs(tp, b, lkey.p, lkey2.p, li, litem2.p, nl, 0, kb, st);
+        }, st, tmp);
+        PG_CK(cudaMemcpyAsync(li, litem2.p, (size_t)nl * sizeof(uint4), cudaMemcpyDeviceToDevice, st));
+    };
     for (size_t k : order) {
         const PieceDev& w = h->work[k];
         const uint32_t nr = w.r1 - w.r0;
-        if (!piece_items[k] && !piece_light[k]) continue;
+        if (!piece_items[k] && !piece_light[k] && !piece_med[k]) continue;
         classify(w, nullptr);
         if (piece_items[k]) {
             k_row_emit<<<grid_for(nr), kThreads, 0, st>>>(w, hf.p, hpos.p, h->d_items.p + base);
             PG_LAUNCH_CHECK();
         }
-        if (piece_light[k]) {
-            uint4* li = h->d_light.p + lbase;
-            k_light_emit<<<grid_for(nr), kThreads, 0, st>>>(w, h->d_tasks.p, lf.p, lpos.p, h->d_col.p, h->d_rowptr.p,
-                                                            li, lkey.p);
-            PG_LAUNCH_CHECK();
-            // the piece's light items by work (stable: rows ascending within equal work)
-            const int64_t nl = (int64_t)piece_light[k];
-            const int kb = 8 + bits_for((uint64_t)(nl - 1) / kLightSortWindow);
-            cub_call([&](void* tp, size_t& b) {
-                return cub::DeviceRadixSort::SortPairs(tp, b, lkey.p, lkey2.p, li, litem2.p, nl, 0, kb, st);
-            }, st, tmp);
-            PG_CK(cudaMemcpyAsync(li, litem2.p, (size_t)nl * sizeof(uint4), cudaMemcpyDeviceToDevice, st));
-        }
+        if (piece_light[k]) emit_light(w, lf.p, lpos.p, h->d_light.p + lbase, (int64_t)piece_light[k]);
+        if (piece_med[k]) emit_light(w, mf.p, mpos.p, h->d_light.p + mbase, (int64_t)piece_med[k]);
         base += piece_items[k];
         lbase += piece_light[k];
+        mbase += piece_med[k];
     }
     PG_CK(cudaStreamSynchronize(st));
 }

@@ -916,11 +916,11 @@ constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
 // is compared with LA held slots, not kLightLa (unused slots are ~0u).
 // STRIDE: the thread takes neighbours e0, e0 + STRIDE, ... (1 in the light kernel;
 // 32 when the lanes of a warp share one row, the heavy kernel's small-held path).
-template <int VM, bool POS, int LA, int STRIDE = 1>
+template <int VM, bool POS, int LA, int STRIDE = 1, int HELD>
 __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowptr,
                                                 const uint32_t* __restrict__ vcol, const uint32_t* __restrict__ npos,
                                                 uint64_t rp_jx, const uint32_t* __restrict__ Bc, uint32_t e0,
-                                                uint32_t e1, const uint32_t (&a)[kLightLa], uint32_t la,
+                                                uint32_t e1, const uint32_t (&a)[HELD], uint32_t la,
                                                 unsigned long long* __restrict__ tvj,
                                                 unsigned long long* __restrict__ tvx) {
     uint32_t acc = 0;
@@ -1261,8 +1261,14 @@ k_tc_rows(const unsigned long long* __restrict__ items, unsigned long long nitem
 // ---------------------------------------------------------------------------
 // items: the whole rank's light items, or one wave's range of them (streaming: the
 // task table and pools then point at the wave's arena).
-template <int VM, bool TIMED>
-__global__ void __launch_bounds__(kLightThreads, PGABB_LIGHT_MINB)
+// HELD: registers for the held ids -- kLightLa (light items), or kMedLa for the
+// medium items (R29), a separate instantiation so that the light one keeps its
+// occupancy.
+#ifndef PGABB_MED_MINB
+#define PGABB_MED_MINB 5
+#endif
+template <int VM, bool TIMED, int HELD>
+__global__ void __launch_bounds__(kLightThreads, HELD > (int)kLightLa ? PGABB_MED_MINB : PGABB_LIGHT_MINB)
 k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
@@ -1307,9 +1313,9 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
         const TaskDev& T = tasks[t];
         const uint64_t col_ij = T.n_col, bm_jx = T.t_bm, npos = T.n_pos;
         const uint32_t* __restrict__ A = col + T.s_col + a0;
-        uint32_t a[kLightLa];
+        uint32_t a[HELD];
 #pragma unroll
-        for (int k = 0; k < (int)kLightLa; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
+        for (int k = 0; k < HELD; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
         const bool row_cr = VM >= 2 || (VM == 1 && T.dir == kDirLow);
         unsigned long long* tvj = (VM >= 2 || (VM == 1 && T.dir == kDirMid)) ? tv + T.c_nbr : nullptr;
         unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
@@ -1322,7 +1328,7 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
                 const uint32_t* __restrict__ row = BM + (uint64_t)v * W;
                 uint32_t c = 0;
 #pragma unroll
-                for (int k = 0; k < (int)kLightLa; ++k)
+                for (int k = 0; k < HELD; ++k)
                     if (k < (int)la) {
                         const uint32_t hit = (__ldg(row + (a[k] >> 5)) >> (a[k] & 31)) & 1u;
                         if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
@@ -1337,13 +1343,13 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
 #define LLISTS(P, L)                                                                                       \
     light_lists<VM, P, L>(col, rowptr, col + col_ij, P ? col + npos : nullptr, T.t_rp, col + T.t_col, e0, e1, a, \
                           la, tvj, tvx)
-            constexpr int kLa8 = kLightLa > 8 ? 8 : (int)kLightLa;   // the 8-wide step when kLightLa > 8
+            constexpr int kLa8 = HELD > 8 ? 8 : HELD;   // the 8-wide step when HELD > 8
             if (npos != ~0ull)
                 acc = lam <= 1 ? LLISTS(true, 1) : lam <= 2 ? LLISTS(true, 2) : lam <= 4 ? LLISTS(true, 4)
-                    : lam <= 8 ? LLISTS(true, kLa8) : LLISTS(true, (int)kLightLa);
+                    : lam <= 8 ? LLISTS(true, kLa8) : LLISTS(true, HELD);
             else
                 acc = lam <= 1 ? LLISTS(false, 1) : lam <= 2 ? LLISTS(false, 2) : lam <= 4 ? LLISTS(false, 4)
-                    : lam <= 8 ? LLISTS(false, kLa8) : LLISTS(false, (int)kLightLa);
+                    : lam <= 8 ? LLISTS(false, kLa8) : LLISTS(false, HELD);
 #undef LLISTS
         }
         acc_t += acc;
@@ -1586,24 +1592,35 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
     };
     auto light_kernel = [&]() {
-        if (timed) return k_tc_light<0, true>;
+        if (timed) return k_tc_light<0, true, kLightLa>;
         switch (vm) {
-            case 1: return k_tc_light<1, false>;
-            case 2: return k_tc_light<2, false>;
-            case 3: return k_tc_light<3, false>;
-            default: return k_tc_light<0, false>;
+            case 1: return k_tc_light<1, false, kLightLa>;
+            case 2: return k_tc_light<2, false, kLightLa>;
+            case 3: return k_tc_light<3, false, kLightLa>;
+            default: return k_tc_light<0, false, kLightLa>;
         }
     };
-    static thread_local int light_dev = -1, light_grid = 0;
+    auto med_kernel = [&]() {
+        if (timed) return k_tc_light<0, true, kMedLa>;
+        switch (vm) {
+            case 1: return k_tc_light<1, false, kMedLa>;
+            case 2: return k_tc_light<2, false, kMedLa>;
+            case 3: return k_tc_light<3, false, kMedLa>;
+            default: return k_tc_light<0, false, kMedLa>;
+        }
+    };
+    static thread_local int light_dev = -1, light_grid = 0, med_grid = 0;
     if (light_dev != h->device) {
         int per_sm = 0;
-        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false>, kLightThreads, 0));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false, kLightLa>, kLightThreads, 0));
         light_grid = sm_count(h->device) * std::max(per_sm, 1);
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_light<0, false, kMedLa>, kLightThreads, 0));
+        med_grid = sm_count(h->device) * std::max(per_sm, 1);
         light_dev = h->device;
     }
-    auto grid_for_light = [&](unsigned long long n) {
+    auto grid_for_light = [&](unsigned long long n, int g) {
         return (unsigned)std::max<unsigned long long>(
-            1ull, std::min<unsigned long long>(light_grid, (n + kLightThreads - 1) / kLightThreads));
+            1ull, std::min<unsigned long long>(g, (n + kLightThreads - 1) / kLightThreads));
     };
 
     PG_NVTX(vtx ? "pgabb_vertex_triangles" : "pgabb_triangle_count");
@@ -1624,7 +1641,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
         PG_CK(cudaMemsetAsync(h->d_task_counts.p, 0, (nt + 1) * sizeof(unsigned long long), st));
         if (vtx) PG_CK(cudaMemsetAsync(tv, 0, (size_t)h->n * sizeof(unsigned long long), st));
-        PG_CK(cudaMemsetAsync(h->d_next.p, 0, 2 * sizeof(unsigned long long), st));
+        PG_CK(cudaMemsetAsync(h->d_next.p, 0, 6 * sizeof(unsigned long long), st));
         PG_CK(cudaEventRecord(h->ev1, st));
         if (h->n_items) {
             rows_kernel()<<<grid_for_items(h->n_items), kRowWarps * 32, smem, st>>>(
@@ -1635,10 +1652,18 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         }
         PG_CK(cudaEventRecord(h->ev_mid, st));
         h->light_timed = true;
-        if (h->n_light) {
-            light_kernel()<<<grid_for_light(h->n_light), kLightThreads, 0, st>>>(
-                h->d_light.p, h->n_light, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p,
+        if (h->n_light0) {
+            light_kernel()<<<grid_for_light(h->n_light0, light_grid), kLightThreads, 0, st>>>(
+                h->d_light.p, h->n_light0, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p,
                 tv, h->d_next.p, timed ? d_cycles + nt : nullptr);
+            PG_LAUNCH_CHECK();
+            h->launches_last++;
+        }
+        if (h->n_light > h->n_light0) {
+            const unsigned long long nm = h->n_light - h->n_light0;
+            med_kernel()<<<grid_for_light(nm, med_grid), kLightThreads, 0, st>>>(
+                h->d_light.p + h->n_light0, nm, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
+                h->d_task_counts.p, tv, h->d_next.p + 5, timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -1683,7 +1708,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             // pointers address the arena
             const uint32_t* base = h->d_arena.p;
             const TaskDev* wt = h->d_wave_tasks.p + wv.task_table * nt;
-            PG_CK(cudaMemsetAsync(h->d_next.p + 2, 0, 2 * sizeof(unsigned long long), st));
+            PG_CK(cudaMemsetAsync(h->d_next.p + 2, 0, 3 * sizeof(unsigned long long), st));
             if (wv.item_end > wv.item_begin) {
                 const unsigned long long ni = wv.item_end - wv.item_begin;
                 rows_kernel()<<<grid_for_items(ni), kRowWarps * 32, smem, st>>>(
@@ -1694,8 +1719,16 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             }
             if (wv.light_end > wv.light_begin) {
                 const unsigned long long nl = wv.light_end - wv.light_begin;
-                light_kernel()<<<grid_for_light(nl), kLightThreads, 0, st>>>(
+                light_kernel()<<<grid_for_light(nl, light_grid), kLightThreads, 0, st>>>(
                     h->d_light.p + wv.light_begin, nl, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 3,
+                    nullptr);
+                PG_LAUNCH_CHECK();
+                h->launches_last++;
+            }
+            if (wv.med_end > wv.med_begin) {
+                const unsigned long long nm = wv.med_end - wv.med_begin;
+                med_kernel()<<<grid_for_light(nm, med_grid), kLightThreads, 0, st>>>(
+                    h->d_light.p + wv.med_begin, nm, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 4,
                     nullptr);
                 PG_LAUNCH_CHECK();
                 h->launches_last++;

@@ -210,6 +210,14 @@ __host__ __device__ inline uint32_t heavy_chunks(uint32_t le) { return (le + kCh
 #define PGABB_LIGHT_LA 8
 #endif
 constexpr uint32_t kLightLa = PGABB_LIGHT_LA;   // |A_ix[u]| <= kLightLa (the register copy)
+// Medium rows: kLightLa < |held| <= kMedLa, otherwise light, go to a second
+// instantiation of the thread-per-row kernel with kMedLa registers for the held ids
+// (its own item list after the light one), so the light kernel keeps its occupancy
+// (build option light_held; DESIGN R29).
+#ifndef PGABB_MED_LA
+#define PGABB_MED_LA 15
+#endif
+constexpr uint32_t kMedLa = PGABB_MED_LA;
 #ifndef PGABB_LIGHT_LE
 #define PGABB_LIGHT_LE 32
 #endif
@@ -227,7 +235,7 @@ constexpr uint32_t kLightWork = PGABB_LIGHT_WORK;   // list loads per row
 //   x = task | |S| << 16 | |nbr| << 20,  y = held rowptr[r],  z = nbr rowptr[r],  w = r
 // (task < 2^16: p <= 64 gives at most C(66,3) = 45760 tasks).
 constexpr uint32_t kLightTaskBits = 16;
-static_assert(kLightLa < 16 && kLightLe < 4096, "light item bit fields");
+static_assert(kLightLa < 16 && kMedLa < 16 && kMedLa >= kLightLa && kLightLe < 4096, "light item bit fields");
 static_assert((kMaxParts + 2) * (kMaxParts + 1) * kMaxParts / 6 < (1u << kLightTaskBits), "task id field");
 __host__ __device__ inline uint32_t light_pair_loads(uint32_t la, uint32_t lb) {
     if (lb <= kLightScan) return lb;
@@ -257,6 +265,7 @@ struct Wave {
     size_t piece_begin = 0, piece_end = 0;   // range of owned pieces (locality order positions)
     uint64_t item_begin = 0, item_end = 0;   // its heavy row items (the build's item list)
     uint64_t light_begin = 0, light_end = 0; // its light row items
+    uint64_t med_begin = 0, med_end = 0;     // its medium row items (in the light list, after n_light0)
     size_t task_table = 0;      // index of this wave's TaskDev table (ntasks entries)
 };
 
@@ -312,10 +321,13 @@ struct pgabb_blocks_s {
     pgabb::DBuf<unsigned long long> d_items;         // heavy row items (warp per row)
     uint64_t n_items = 0;
     pgabb::DBuf<uint4> d_light;                      // light row items (thread per row, DESIGN R20)
-    uint64_t n_light = 0;
+    uint64_t n_light = 0;                            // light + medium items
+    uint64_t n_light0 = 0;                           // [0, n_light0) light, [n_light0, n_light) medium
+    uint32_t light_held = pgabb::kLightLa;           // largest held list of a thread-per-row item (8 or 15)
+    bool light_auto = false;                         // light_held chosen by the build (R29)
     // item offsets per owned piece in locality order (size pieces + 1): the waves of
     // streaming residency take contiguous ranges of them
-    std::vector<uint64_t> piece_item_off, piece_light_off;
+    std::vector<uint64_t> piece_item_off, piece_light_off, piece_med_off;
     pgabb::DBuf<unsigned long long> d_task_counts;   // ntasks (+1 total at the end)
     pgabb::DBuf<unsigned long long> d_next;          // dynamic scheduling counters
 

@@ -46,11 +46,30 @@ def test_binding_matches_header():
     assert sorted(n for n, _, _ in _abi.SIGNATURES) == declared()
 
 
-def test_struct_layouts():
+def test_struct_layouts(tmp_path):
+    # the ctypes mirrors against the C compiler's layout of include/pgabb.h
     from paper_2209_04541_b200 import _abi
-    assert ctypes.sizeof(_abi.BuildOpts) == 72
-    assert ctypes.sizeof(_abi.CountOpts) == 32
-    assert ctypes.sizeof(_abi.Stats) == 21 * 8 + 6 * 8   # + ms_cc_last took a reserved double   # 17 counters + items_heavy/light, alg_bytes_light, d2d_bytes_last; 6 doubles
+    structs = {"BuildOpts": "pgabb_build_opts_t", "CountOpts": "pgabb_count_opts_t", "Stats": "pgabb_stats_t"}
+    lines = []
+    for py, c in structs.items():
+        cls = getattr(_abi, py)
+        lines.append(f'printf("{py} size %zu\\n", sizeof({c}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{py} {f} %zu\\n", offsetof({c}, {f}));')
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"pgabb.h\"\nint main(void){"
+                   + "".join(lines) + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = {}
+    for ln in subprocess.check_output([str(exe)]).decode().splitlines():
+        py, f, v = ln.split()
+        got[(py, f)] = int(v)
+    for py in structs:
+        cls = getattr(_abi, py)
+        assert got[(py, "size")] == ctypes.sizeof(cls), py
+        for f, _ in cls._fields_:
+            assert got[(py, f)] == getattr(cls, f).offset, (py, f)
 
 
 def test_sm100a_cubin(lib_path):

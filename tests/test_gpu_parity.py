@@ -272,3 +272,41 @@ def test_max_parts_and_clamp():
     small = gen.complete(5)
     with pg.build_blocks(*small, p=40) as b:             # p > n is clamped to n (R7)
         assert b.stats()["p"] == 5 and b.triangle_count() == 10
+
+
+# ------------------------------------------- medium thread-per-row items (R29)
+@pytest.mark.parametrize("p", [2, 4])
+def test_light_held_classes(p):
+    # ER at p = 2 / 4 holds many rows with 9..15 ids per block row: with
+    # light_held = 15 they run in the medium kernel instead of heavy warp items
+    for g in (gen.er(1 << 15, 32, seed=21), gen.rmat(13, 16, seed=22)):
+        want = oracle.count(*g)
+        res = {}
+        for lh in (8, 15, 0):
+            with pg.build_blocks(*g, p=p, light_held=lh) as b:
+                T, tc = b.triangle_count(task_counts=True)
+                st = b.stats()
+            assert T == want
+            res[lh] = (tc, st["items_heavy"], st["items_light"])
+        assert (res[8][0] == res[15][0]).all()
+        assert res[15][2] >= res[8][2] and res[15][1] <= res[8][1]
+    # the ER case really moves rows into the medium list
+    g = gen.er(1 << 15, 32, seed=21)
+    with pg.build_blocks(*g, p=p, light_held=8) as b8, pg.build_blocks(*g, p=p, light_held=15) as b15:
+        s8, s15 = b8.stats(), b15.stats()
+        assert s15["items_light"] > s8["items_light"] and s8["items_medium"] == 0
+        assert s15["items_light"] - s15["items_medium"] == s8["items_light"]
+        assert (s8["light_held"], s15["light_held"]) == (8, 15)
+
+
+def test_light_held_streaming_and_rejects():
+    g = gen.er(1 << 14, 32, seed=23)
+    want = oracle.count(*g)
+    with pg.build_blocks(*g, p=4, light_held=15) as ref:
+        mt = ref.stats()["max_task_bytes"]
+    with pg.build_blocks(*g, p=4, light_held=15, residency=pg.RESIDENT_HOST, device_budget_bytes=int(5 * mt)) as b:
+        assert b.stats()["waves"] > 1
+        assert b.triangle_count() == want
+    with pytest.raises(pg.PgabbError) as e:
+        pg.build_blocks(*g, p=4, light_held=9)
+    assert e.value.name == "EINVAL"

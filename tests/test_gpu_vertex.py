@@ -65,6 +65,13 @@ def test_er_grid_per_vertex():
     check(gen.grid(300, 0.3, seed=4), p=6)
 
 
+@pytest.mark.parametrize("light_held", [8, 15])
+def test_per_vertex_light_held(light_held):
+    # medium thread-per-row items (R29) credit u, v and w like the light ones
+    check(gen.er(1 << 14, 32, seed=5), p=2, light_held=light_held)
+    check(gen.rmat(13, 16, seed=6), p=4, light_held=light_held)
+
+
 def test_wide_parts_hash_and_search_paths():
     # p=1 over n > 32768 ids: the column part is wider than the warp bitmap, so
     # rows use the hash set (|A_ix[u]| <= 512) or binary search (> 512: K_700)
