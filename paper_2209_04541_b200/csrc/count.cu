@@ -906,6 +906,23 @@ constexpr bool kLightPrefetch = PGABB_LIGHT_PREFETCH;
 #define PGABB_LIGHT_VPIPE 1
 #endif
 constexpr bool kLightVPipe = PGABB_LIGHT_VPIPE;
+#ifndef PGABB_LIGHT_VEC
+#define PGABB_LIGHT_VEC 0   // A/B: c3 p=4 -1 %, p=8 +5 %, c4 +31 %
+#endif
+constexpr bool kLightVec = PGABB_LIGHT_VEC;   // scanned lists read as aligned 16-byte chunks
+#ifndef PGABB_LIGHT_CS
+#define PGABB_LIGHT_CS 0
+#endif
+constexpr bool kLightCs = PGABB_LIGHT_CS;   // light items / held / neighbour ids loaded evict-first (ld.global.cs)
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+    if constexpr (kLightCs) return __ldcs(p);
+    else return __ldg(p);
+}
+#ifndef PGABB_LIGHT_AVEC
+#define PGABB_LIGHT_AVEC 0
+#endif
+constexpr bool kLightAVec = PGABB_LIGHT_AVEC;   // held ids (<= 8) read as aligned 16-byte chunks
 
 // The list branch of a light row: for each neighbour v (vcol[e0..e1)) its streamed
 // list Bc[b0..b1) -- from rowptr, or (POS: MID tasks with x == j) from after the
@@ -926,7 +943,7 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
     uint32_t acc = 0;
     uint32_t vn = 0, bn0 = 0, bn1 = 0;
     if (kLightVPipe && e0 < e1) {
-        vn = __ldg(vcol + e0);
+        vn = STRIDE == 1 ? ld_stream(vcol + e0) : __ldg(vcol + e0);
         bn0 = POS ? __ldg(npos + e0) + 1 : __ldg(rowptr + rp_jx + vn);
         bn1 = __ldg(rowptr + rp_jx + vn + 1);
     }
@@ -937,7 +954,7 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
             b0 = bn0;
             b1 = bn1;
             if (e + STRIDE < e1) {
-                vn = __ldg(vcol + e + STRIDE);
+                vn = STRIDE == 1 ? ld_stream(vcol + e + STRIDE) : __ldg(vcol + e + STRIDE);
                 bn0 = POS ? __ldg(npos + e + STRIDE) + 1 : __ldg(rowptr + rp_jx + vn);
                 bn1 = __ldg(rowptr + rp_jx + vn + 1);
             }
@@ -948,7 +965,29 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
         }
         const uint32_t lb = b1 - b0;
         uint32_t c = 0;
-        if (lb <= kLightScan) {
+        if (kLightVec && STRIDE == 1 && lb <= kLightScan) {
+            // the list's aligned 16-byte chunks (one L2 request each instead of one per
+            // id; the pools are padded, so a chunk never leaves the allocation); ids
+            // outside [b0, b1) are masked out of the hits
+            const uintptr_t pa = reinterpret_cast<uintptr_t>(Bc + b0);
+            const uint4* c4 = reinterpret_cast<const uint4*>(pa & ~(uintptr_t)15);
+            const int off = (int)((pa >> 2) & 3);
+            const int nch = (off + (int)lb + 3) >> 2;
+            for (int ch = 0; ch < nch; ++ch) {
+                const uint4 w4 = __ldg(c4 + ch);
+                const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int idx = 4 * ch + j - off;
+                    uint32_t hit = 0;
+#pragma unroll
+                    for (int k = 0; k < LA; ++k) hit |= (ws[j] == a[k]);
+                    hit &= (uint32_t)(idx >= 0 && idx < (int)lb);
+                    if (VM >= 3 && hit) atomicAdd(tvx + ws[j], 1ull);
+                    c += hit;
+                }
+            }
+        } else if (lb <= kLightScan) {
             for (uint32_t q = b0; q < b1; ++q) {
                 const uint32_t x = __ldg(Bc + q);
                 uint32_t hit = 0;
@@ -1283,16 +1322,16 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= nitems) break;
     uint4 it_next = make_uint4(0, 0, 0, 0);   // PGABB_LIGHT_PREFETCH: the next item, loaded a step early
-    if (kLightPrefetch && base + lane < nitems) it_next = __ldg(items + base + lane);
+    if (kLightPrefetch && base + lane < nitems) it_next = ld_stream(items + base + lane);
     for (int r = 0; r < kLightChunk; ++r) {
         const unsigned long long idx = base + 32 * r + lane;
         if (idx >= nitems) break;
         uint4 it;
         if (kLightPrefetch) {
             it = it_next;
-            if (r + 1 < kLightChunk && idx + 32 < nitems) it_next = __ldg(items + idx + 32);
+            if (r + 1 < kLightChunk && idx + 32 < nitems) it_next = ld_stream(items + idx + 32);
         } else {
-            it = __ldg(items + idx);
+            it = ld_stream(items + idx);
         }
         const uint32_t t = it.x & ((1u << kLightTaskBits) - 1);
         const uint32_t u = it.w;
@@ -1314,8 +1353,33 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
         const uint64_t col_ij = T.n_col, bm_jx = T.t_bm, npos = T.n_pos;
         const uint32_t* __restrict__ A = col + T.s_col + a0;
         uint32_t a[HELD];
+        if (kLightAVec && HELD <= 8) {
+            // the held ids from their aligned 16-byte chunks (<= 3 loads instead of one
+            // per id), shifted into place by the list's offset within its first chunk
+            constexpr int kCh = (HELD + 6) / 4;
+            const uintptr_t pa = reinterpret_cast<uintptr_t>(A);
+            const uint4* c4 = reinterpret_cast<const uint4*>(pa & ~(uintptr_t)15);
+            const int off = (int)((pa >> 2) & 3);
+            const int nch = (off + (int)la + 3) >> 2;
+            uint32_t w[4 * kCh];
 #pragma unroll
-        for (int k = 0; k < HELD; ++k) a[k] = (k < (int)la) ? __ldg(A + k) : 0xffffffffu;
+            for (int ch = 0; ch < kCh; ++ch) {
+                uint4 w4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (ch < nch) w4 = __ldg(c4 + ch);
+                w[4 * ch] = w4.x;
+                w[4 * ch + 1] = w4.y;
+                w[4 * ch + 2] = w4.z;
+                w[4 * ch + 3] = w4.w;
+            }
+#pragma unroll
+            for (int k = 0; k < HELD; ++k) {
+                const uint32_t x = off == 0 ? w[k] : off == 1 ? w[k + 1] : off == 2 ? w[k + 2] : w[k + 3];
+                a[k] = (k < (int)la) ? x : 0xffffffffu;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < HELD; ++k) a[k] = (k < (int)la) ? ld_stream(A + k) : 0xffffffffu;
+        }
         const bool row_cr = VM >= 2 || (VM == 1 && T.dir == kDirLow);
         unsigned long long* tvj = (VM >= 2 || (VM == 1 && T.dir == kDirMid)) ? tv + T.c_nbr : nullptr;
         unsigned long long* tvx = VM > 0 ? tv + T.cx : nullptr;
