@@ -23,6 +23,31 @@ def to_bytes(s):
     return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[u]
 
 
+def aggregate(ks):
+    """One summary over launches of several instantiations (sums and time-weighted ratios)."""
+    def num(d, q):
+        return float(str(d.get(q, "0 x")).split()[0] or 0)
+    def unit(d, q):
+        parts = str(d.get(q, "")).split()
+        return parts[1] if len(parts) > 1 else ""
+    t = [num(d, "gpu__time_duration.sum") * {"ms": 1.0, "s": 1e3, "us": 1e-3}.get(unit(d, "gpu__time_duration.sum"), 1.0)
+         for d in ks]
+    T = sum(t) or 1.0
+    out = dict(ks[0])
+    out["kernel"] = " + ".join(d["kernel"] for d in ks)
+    out["gpu__time_duration.sum"] = f"{sum(t)} ms"
+    for q in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        out[q] = f"{sum(to_bytes(d[q]) for d in ks)} byte"
+    out["smsp__inst_executed.sum"] = f"{sum(num(d, 'smsp__inst_executed.sum') for d in ks)} inst"
+    for q in list(out):
+        if q.endswith(".pct") or q.endswith("pct_of_peak_sustained_active") or q.startswith("smsp__pcsamp"):
+            try:
+                out[q] = f"{sum(num(d, q) * ti for d, ti in zip(ks, t)) / T} {unit(ks[0], q)}"
+            except Exception:
+                pass
+    return out
+
+
 def main(tag, config, rnd="01", src_hash=None):
     """src_hash: bench.kernel_src_hash() of the sources the capture ran (default: now)."""
     if src_hash is None:
@@ -54,6 +79,14 @@ def main(tag, config, rnd="01", src_hash=None):
             if not ks:
                 continue
             k = ks[0]
+            # several instantiations of one kernel in one count (k_tc_light<.., 8> and the
+            # medium <.., 15>, R29): the capture must hold one launch of each; their DRAM
+            # bytes, times and instructions add, ratios are time-weighted
+            inst = {}
+            for d in ks:
+                inst.setdefault(d["kernel"], d)
+            if len(inst) > 1:
+                k = aggregate(list(inst.values()))
             out[f"ncu_{kname}"] = k
             traffic = to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"])
             out[f"dram_bytes_per_launch_{kname}"] = traffic
