@@ -440,6 +440,10 @@ __device__ __forceinline__ uint32_t streamed_len(const TaskDev& T, const uint32_
 
 // held_max: kLightLa, or kMedLa when medium rows (kLightLa < |S| <= kMedLa, R29) get
 // mf = 1 for the second thread-per-row kernel instead of heavy items.
+#ifndef PGABB_MED_LONG
+#define PGABB_MED_LONG 0
+#endif
+constexpr bool kMedLong = PGABB_MED_LONG;   // medium rows may binary-search long lists (A/B)
 __global__ void k_row_flags(PieceDev w, const TaskDev* tasks, const uint32_t* col, const uint32_t* rowptr,
                             uint32_t* hf, uint32_t* lf, uint32_t* mf, uint32_t held_max, unsigned long long* alg) {
     const TaskDev T = tasks[w.task];
@@ -466,7 +470,7 @@ __global__ void k_row_flags(PieceDev w, const TaskDev* tasks, const uint32_t* co
                     // a medium row only when every streamed list is a short scanned list (no
                     // per-id binary searches, no dense block: R-MAT rows against hub lists
                     // or bitmaps stay heavy warp items, R29)
-                    if (la > kLightLa && (T.t_bm != ~0ull || lmax > kLightScan)) light = false;
+                    if (la > kLightLa && (T.t_bm != ~0ull || (!kMedLong && lmax > kLightScan))) light = false;
                     bytes = 4ull * (la + lsum) + 12ull * (e1 - e0);
                 }
                 fl = light && la <= kLightLa;
