@@ -255,6 +255,7 @@ typedef struct {
                                            of the last count (runs concurrently with the GPU) */
     uint64_t items_medium;              /* of items_light: the medium ones (9..15 held ids, R29) */
     uint64_t light_held;                /* the build's light_held (8 or 15; auto resolved) */
+    uint64_t ell_bytes;                 /* device bytes of sector-aligned row slots (DESIGN R30) */
 } pgabb_stats_t;
 
 PGABB_API pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* stats);

@@ -51,7 +51,7 @@ class Stats(ctypes.Structure):
                 ("alg_bytes_light", u64), ("d2d_bytes_last", u64), ("ms_build", ctypes.c_double),
                 ("ms_count_last", ctypes.c_double), ("ms_main_kernel_last", ctypes.c_double),
                 ("ms_light_kernel_last", ctypes.c_double), ("ms_cc_last", ctypes.c_double),
-                ("ms_host_last", ctypes.c_double), ("items_medium", u64), ("light_held", u64)]
+                ("ms_host_last", ctypes.c_double), ("items_medium", u64), ("light_held", u64), ("ell_bytes", u64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("reserved")}

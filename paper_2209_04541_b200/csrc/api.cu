@@ -74,6 +74,7 @@ pgabb_blocks_s::~pgabb_blocks_s() {
     d_tasks.release();
     d_items.release();
     d_light.release();
+    d_ell.release();
     d_deg.release();
     d_tv_rank.release();
     h_result.release();
@@ -317,6 +318,7 @@ pgabb_status_t pgabb_get_stats(pgabb_blocks_t b, pgabb_stats_t* s) {
         s->items_light = b->n_light;
         s->items_medium = b->n_light - b->n_light0;
         s->light_held = b->light_held;
+        s->ell_bytes = b->d_ell.bytes();
         s->alg_bytes_light = b->alg_light;
         s->d2d_bytes_last = b->d2d_last;
     });

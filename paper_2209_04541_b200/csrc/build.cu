@@ -420,6 +420,25 @@ __global__ void k_fill_bitmap(const uint32_t* col, const uint32_t* rowptr, unsig
     }
 }
 
+#ifndef PGABB_ELL
+#define PGABB_ELL 1
+#endif
+constexpr bool kEll = PGABB_ELL;
+// R30: the sector-aligned copy of a short-list block -- row r's slot of ew words is
+// [|row|, first ew-1 ids, 0 ...] at ell + r * ew (64-byte aligned for ew = 16), so a
+// thread reads one aligned segment per pair instead of a rowptr sector and 1-2 list
+// sectors; longer rows continue in the col pool after their first ew-1 ids.
+__global__ void k_fill_ell(const uint32_t* col, const uint32_t* rowptr, uint64_t col_off, uint64_t rp_off,
+                           uint32_t nrows, uint32_t ew, uint32_t* ell) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nrows;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e0 = rowptr[rp_off + r], e1 = rowptr[rp_off + r + 1];
+        uint32_t* slot = ell + r * ew;
+        slot[0] = e1 - e0;
+        for (uint32_t q = 1; q < ew; ++q) slot[q] = (e0 + q - 1 < e1) ? col[col_off + e0 + q - 1] : 0u;
+    }
+}
+
 // Row items of one owned piece, in kernel roles (TaskDev, R25): rows r in [r0, r1)
 // with a non-empty held list S and neighbour list, classified by their work
 // (DESIGN R20): LIGHT rows -- |S| <= kLightLa, <= kLightLe neighbours and at most
@@ -1117,6 +1136,7 @@ template <class Off>
 static TaskDev make_taskdev(const pgabb_blocks_s* h, const Task& T, Off off) {
     const uint32_t p = h->p, bij = T.i * p + T.j, bix = T.i * p + T.x, bjx = T.j * p + T.x;
     TaskDev d{};
+    d.t_ell = ~0ull;
     d.dir = T.dir;
     d.wx = h->cuts[T.x + 1] - h->cuts[T.x];
     d.cx = h->cuts[T.x];
@@ -1554,6 +1574,48 @@ void upload_work(pgabb_blocks_s* h) {
         base += piece_items[k];
         lbase += piece_light[k];
         mbase += piece_med[k];
+    }
+    // R30: sector-aligned slots for the streamed blocks of this rank's LOW list tasks,
+    // on device-resident handles of graphs that use the medium kernel (short lists
+    // of several sectors: ER-like); the task table then points at them
+    if (kEll && h->residency == PGABB_RESIDENT_DEVICE && h->n_light > h->n_light0) {
+        const uint32_t p = h->p;
+        std::vector<uint64_t> ell_off(h->blocks.size(), ~0ull);
+        std::vector<uint32_t> ell_w(h->blocks.size(), 0);
+        uint64_t words = 0;
+        for (size_t t = 0; t < h->tasks.size(); ++t) {
+            const Task& T = h->tasks[t];
+            if (!task_mine[t] || T.dir != kDirLow || td[t].t_bm != ~0ull) continue;
+            const uint32_t bjx = T.j * p + T.x;
+            const BlockInfo& b = h->blocks[bjx];
+            if (ell_off[bjx] != ~0ull || !b.present || b.nrows == 0) continue;
+            const double avg = (double)b.nnz / b.nrows;
+            const uint32_t ew = avg <= 3.5 ? 8u : (avg <= 10.0 ? 16u : 0u);
+            if (!ew) continue;
+            words = (words + 15) & ~15ull;   // 64-byte aligned slots
+            ell_off[bjx] = words;
+            ell_w[bjx] = ew;
+            words += (uint64_t)b.nrows * ew;
+        }
+        if (words) {
+            h->d_ell.alloc(words + 16);
+            for (size_t bx = 0; bx < h->blocks.size(); ++bx) {
+                if (ell_off[bx] == ~0ull) continue;
+                const BlockInfo& b = h->blocks[bx];
+                k_fill_ell<<<grid_for(b.nrows), kThreads, 0, st>>>(h->d_col.p, h->d_rowptr.p, b.col_off, b.rp_off,
+                                                                   b.nrows, ell_w[bx], h->d_ell.p + ell_off[bx]);
+                PG_LAUNCH_CHECK();
+            }
+            for (size_t t = 0; t < h->tasks.size(); ++t) {
+                const Task& T = h->tasks[t];
+                if (!task_mine[t] || T.dir != kDirLow || td[t].t_bm != ~0ull) continue;
+                const uint32_t bjx = T.j * p + T.x;
+                if (ell_off[bjx] == ~0ull) continue;
+                td[t].t_ell = ell_off[bjx];
+                td[t].ell_w = ell_w[bjx];
+            }
+            PG_COPY_SYNC(h->d_tasks.p, td.data(), td.size() * sizeof(TaskDev), st);
+        }
     }
     PG_CK(cudaStreamSynchronize(st));
 }

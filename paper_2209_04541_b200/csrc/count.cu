@@ -1016,6 +1016,76 @@ __device__ __forceinline__ uint32_t light_lists(const uint32_t* __restrict__ col
     return acc;
 }
 
+// R30: the list branch over the streamed block's sector-aligned slots (LOW tasks of
+// device-resident ER-like graphs): one aligned EW-word segment per neighbour v holds
+// |A_jx[v]| and its first EW-1 ids, compared with the held ids; a longer list goes
+// on in the col pool after its first EW-1 ids (scanned, or binary-searched per held
+// id when long).  The next neighbour id is loaded while the current slot is used.
+template <int VM, int LA, int EW, int HELD>
+__device__ __forceinline__ uint32_t light_ell(const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ vcol,
+                                              uint64_t rp_jx, const uint32_t* __restrict__ Bc,
+                                              const uint32_t* __restrict__ ell, uint32_t e0, uint32_t e1,
+                                              const uint32_t (&a)[HELD], uint32_t la,
+                                              unsigned long long* __restrict__ tvj,
+                                              unsigned long long* __restrict__ tvx) {
+    uint32_t acc = 0;
+    uint32_t vn = e0 < e1 ? __ldg(vcol + e0) : 0u;
+    for (uint32_t e = e0; e < e1; ++e) {
+        const uint32_t v = vn;
+        if (e + 1 < e1) vn = __ldg(vcol + e + 1);
+        const uint4* sp = reinterpret_cast<const uint4*>(ell + (uint64_t)v * EW);
+        uint32_t w[EW];
+#pragma unroll
+        for (int q = 0; q < EW / 4; ++q) {
+            const uint4 x = __ldg(sp + q);
+            w[4 * q] = x.x;
+            w[4 * q + 1] = x.y;
+            w[4 * q + 2] = x.z;
+            w[4 * q + 3] = x.w;
+        }
+        const uint32_t len = w[0];
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 1; j < EW; ++j) {
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < LA; ++k) hit |= (w[j] == a[k]);
+            hit &= (uint32_t)((uint32_t)j <= len);
+            if (VM >= 3 && hit) atomicAdd(tvx + w[j], 1ull);
+            c += hit;
+        }
+        if (len > (uint32_t)(EW - 1)) {   // the rest of a long list, from the col pool
+            const uint32_t b0 = __ldg(rowptr + rp_jx + v) + (EW - 1), b1 = __ldg(rowptr + rp_jx + v + 1);
+            if (b1 - b0 <= kLightScan) {
+                for (uint32_t q = b0; q < b1; ++q) {
+                    const uint32_t x = __ldg(Bc + q);
+                    uint32_t hit = 0;
+#pragma unroll
+                    for (int k = 0; k < LA; ++k) hit |= (x == a[k]);
+                    if (VM >= 3 && hit) atomicAdd(tvx + x, 1ull);
+                    c += hit;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < LA; ++k)
+                    if (k < (int)la) {
+                        uint32_t lo = b0, hi = b1;
+                        while (lo < hi) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (__ldg(Bc + mid) < a[k]) lo = mid + 1; else hi = mid;
+                        }
+                        const uint32_t hit = (lo < b1 && __ldg(Bc + lo) == a[k]);
+                        if (VM >= 3 && hit) atomicAdd(tvx + a[k], 1ull);
+                        c += hit;
+                    }
+            }
+        }
+        acc += c;
+        if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
+    }
+    return acc;
+}
+
 // items[] holds the row items in locality order: the whole rank's (device-resident
 // blocks) or one wave's range of them (streaming residency: the task table and the
 // pool pointers then all point at the wave's staging arena).
@@ -1311,6 +1381,7 @@ __global__ void __launch_bounds__(kLightThreads, HELD > (int)kLightLa ? PGABB_ME
 k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
            const TaskDev* __restrict__ tasks, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ bitmap,
+           const uint32_t* __restrict__ ell,
            unsigned long long* __restrict__ task_counts, unsigned long long* __restrict__ tv,
            unsigned long long* __restrict__ next, unsigned long long* __restrict__ cyc) {
     const int lane = threadIdx.x & 31;
@@ -1401,6 +1472,19 @@ k_tc_light(const uint4* __restrict__ items, unsigned long long nitems,
                 acc += c;
                 if (VM >= 1 && tvj && c) atomicAdd(tvj + v, (unsigned long long)c);
             }
+        } else if (T.t_ell != ~0ull) {
+            // R30 slots (LOW tasks only: no suffix starts); compare width as below
+            const uint32_t lam = __reduce_max_sync(__activemask(), la);
+            const uint32_t* __restrict__ E = ell + T.t_ell;
+            const uint32_t* __restrict__ Bc = col + T.t_col;
+            const uint32_t* __restrict__ vc_ = col + col_ij;
+            constexpr int kLa8 = HELD > 8 ? 8 : HELD;
+#define LELL(W, L) light_ell<VM, L, W>(rowptr, vc_, T.t_rp, Bc, E, e0, e1, a, la, tvj, tvx)
+            if (T.ell_w == 8)
+                acc = lam <= 2 ? LELL(8, 2) : lam <= 4 ? LELL(8, 4) : lam <= 8 ? LELL(8, kLa8) : LELL(8, HELD);
+            else
+                acc = lam <= 2 ? LELL(16, 2) : lam <= 4 ? LELL(16, 4) : lam <= 8 ? LELL(16, kLa8) : LELL(16, HELD);
+#undef LELL
         } else {
             // the warp's largest held list picks the compare width (warp-uniform)
             const uint32_t lam = __reduce_max_sync(__activemask(), la);
@@ -1718,8 +1802,8 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
         h->light_timed = true;
         if (h->n_light0) {
             light_kernel()<<<grid_for_light(h->n_light0, light_grid), kLightThreads, 0, st>>>(
-                h->d_light.p, h->n_light0, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p, h->d_task_counts.p,
-                tv, h->d_next.p, timed ? d_cycles + nt : nullptr);
+                h->d_light.p, h->n_light0, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p, h->d_ell.p,
+                h->d_task_counts.p, tv, h->d_next.p, timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -1727,7 +1811,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             const unsigned long long nm = h->n_light - h->n_light0;
             med_kernel()<<<grid_for_light(nm, med_grid), kLightThreads, 0, st>>>(
                 h->d_light.p + h->n_light0, nm, h->d_tasks.p, h->d_col.p, h->d_rowptr.p, h->d_bitmap.p,
-                h->d_task_counts.p, tv, h->d_next.p + 5, timed ? d_cycles + nt : nullptr);
+                h->d_ell.p, h->d_task_counts.p, tv, h->d_next.p + 5, timed ? d_cycles + nt : nullptr);
             PG_LAUNCH_CHECK();
             h->launches_last++;
         }
@@ -1784,7 +1868,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             if (wv.light_end > wv.light_begin) {
                 const unsigned long long nl = wv.light_end - wv.light_begin;
                 light_kernel()<<<grid_for_light(nl, light_grid), kLightThreads, 0, st>>>(
-                    h->d_light.p + wv.light_begin, nl, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 3,
+                    h->d_light.p + wv.light_begin, nl, wt, base, base, base, nullptr, h->d_task_counts.p, tv, h->d_next.p + 3,
                     nullptr);
                 PG_LAUNCH_CHECK();
                 h->launches_last++;
@@ -1792,7 +1876,7 @@ uint64_t count_triangles(pgabb_blocks_s* h, const pgabb_count_opts_t* opts, bool
             if (wv.med_end > wv.med_begin) {
                 const unsigned long long nm = wv.med_end - wv.med_begin;
                 med_kernel()<<<grid_for_light(nm, med_grid), kLightThreads, 0, st>>>(
-                    h->d_light.p + wv.med_begin, nm, wt, base, base, base, h->d_task_counts.p, tv, h->d_next.p + 4,
+                    h->d_light.p + wv.med_begin, nm, wt, base, base, base, nullptr, h->d_task_counts.p, tv, h->d_next.p + 4,
                     nullptr);
                 PG_LAUNCH_CHECK();
                 h->launches_last++;

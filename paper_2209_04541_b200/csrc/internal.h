@@ -179,8 +179,11 @@ struct TaskDev {
     uint32_t bm_words;       // words per dense row of the streamed block
     uint32_t c_row, c_nbr, cx;   // rank-space first vertex of the row's, the neighbours' and part x
     uint32_t dir;
+    uint64_t t_ell;          // sector-aligned slots of the streamed block (R30), ~0 if none
+    uint32_t ell_w;          // words per slot (8 or 16): [length, ids...]
+    uint32_t pad_;
 };
-static_assert(sizeof(TaskDev) == 88, "TaskDev layout");
+static_assert(sizeof(TaskDev) == 104, "TaskDev layout");
 
 // A block gets a dense bitmap copy (rows of ceil(w/32) words) when its density is
 // at least 1/kDenseInv and its column part is narrow enough for a warp bitmap:
@@ -300,6 +303,7 @@ struct pgabb_blocks_s {
     pgabb::DBuf<uint32_t> d_col;                // col pool (local col ids), block-major
     pgabb::DBuf<uint32_t> d_rowptr;             // rowptr pool (block-local edge offsets)
     pgabb::DBuf<uint32_t> d_bitmap;             // dense-block bitmap pool (rows of bm_words)
+    pgabb::DBuf<uint32_t> d_ell;                // sector-aligned row slots of short-list blocks (R30)
     pgabb::HBuf<uint32_t> h_col, h_rowptr, h_bitmap;   // host-resident copies (RESIDENT_HOST)
     // RESIDENT_HOST without a budget: the pool ranges of the blocks this rank's pieces
     // read (merged), copied host->device by every count (S9) -- a rank never copies

@@ -297,6 +297,8 @@ def test_light_held_classes(p):
         assert s15["items_light"] > s8["items_light"] and s8["items_medium"] == 0
         assert s15["items_light"] - s15["items_medium"] == s8["items_light"]
         assert (s8["light_held"], s15["light_held"]) == (8, 15)
+        # R30 slots only with medium rows on a device-resident handle
+        assert s8["ell_bytes"] == 0 and s15["ell_bytes"] > 0
 
 
 def test_light_held_streaming_and_rejects():
@@ -305,8 +307,27 @@ def test_light_held_streaming_and_rejects():
     with pg.build_blocks(*g, p=4, light_held=15) as ref:
         mt = ref.stats()["max_task_bytes"]
     with pg.build_blocks(*g, p=4, light_held=15, residency=pg.RESIDENT_HOST, device_budget_bytes=int(5 * mt)) as b:
-        assert b.stats()["waves"] > 1
+        assert b.stats()["waves"] > 1 and b.stats()["ell_bytes"] == 0
         assert b.triangle_count() == want
+    with pg.build_blocks(*g, p=4, light_held=15, residency=pg.RESIDENT_HOST) as b:
+        assert b.stats()["ell_bytes"] == 0
+        assert b.triangle_count() == want
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_ell_slots_long_rows(p):
+    # R30: rows longer than a slot continue in the col pool (scanned or binary-
+    # searched); ER d = 48 at p = 1 / 3 puts many rows past 15 ids
+    g = gen.er(1 << 14, 48, seed=24)
+    want = oracle.count(*g)
+    with pg.build_blocks(*g, p=p, light_held=15) as b:
+        T, tc = b.triangle_count(task_counts=True)
+        st = b.stats()
+    with pg.build_blocks(*g, p=p, light_held=8) as b8:
+        T8, tc8 = b8.triangle_count(task_counts=True)
+    assert T == T8 == want and (tc == tc8).all()
+    if p == 3:   # blocks of ~8 ids per row get 16-word slots (p = 1: ~24 per row, none)
+        assert st["items_medium"] > 0 and st["ell_bytes"] > 0
     with pytest.raises(pg.PgabbError) as e:
         pg.build_blocks(*g, p=4, light_held=9)
     assert e.value.name == "EINVAL"
