@@ -525,7 +525,8 @@ def run_ours(args):
                            clocks.get("sm_mhz") or 1965.0, torch.cuda.get_device_properties(dev).multi_processor_count)
     roofline["s10_combined"] = kern("k_tc_rows + k_tc_light", kms, alg)
     roofline["items"] = {"heavy": int(st["items_heavy"]), "light": int(st["items_light"]),
-                         "medium": int(st["items_medium"]), "light_held": int(st["light_held"])}
+                         "medium": int(st["items_medium"]), "light_held": int(st["light_held"]),
+                         "ell_bytes": int(st["ell_bytes"])}
 
     # e2e: host-resident handle through the same public call, H2D inside the timed region
     e2e = None
